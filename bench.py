@@ -1,0 +1,370 @@
+"""SMoE MLP fwd+bwd benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1|C2|C0] [--impl ours|reference]
+
+A step = one pass of the ParallelLinear hot path over one batch: the routing
+sort (flatten_and_sort), smoe_mlp_forward(training=True) and
+smoe_mlp_backward, at the configuration BASELINE.json's metric is quoted on
+(configs[1], "C1": Mixtral-8x7B MLP layer, T=32768, d_model=4096,
+d_expert=14336, E=8, k=2, bf16).  Inputs are synthetic, weights random-init;
+routing is a softmax gate + stable top-k computed once outside the timed
+region (as the reference bench does, bench.py:120-130).
+
+value  : tokens/s with inputs resident in HBM (device time, CUDA events).
+e2e    : the same step through the public API from pinned HOST buffers:
+         X, dY, expert ids and p copied H2D, dX and dp copied D2H, inside the
+         timed region.
+roofline: the dominant kernel (the layer-1 forward grouped GEMM) timed alone
+         with CUDA events on its stream; algorithmic FLOPs = 2*T*k*d*d_e.
+cpu_baseline: the CPU oracle (NumPy restatement of the reference, oracle/)
+         on a bounded sample (T=128 at C1 dims), rank 0 at N=1 only.
+--impl reference: the same metric from the oracle port on the host CPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (T, d_model, d_expert, E, k, description)
+    "C0": (4096, 512, 1024, 8, 2, "C0 oracle config: T=4096, d_model=512, d_expert=1024, E=8, k=2"),
+    "C1": (32768, 4096, 14336, 8, 2,
+           "C1 Mixtral-8x7B MLP layer: T=32768, d_model=4096, d_expert=14336, E=8, k=2, gelu, fwd+bwd"),
+    "C2": (32768, 4096, 1792, 64, 8,
+           "C2 fine-grained: T=32768, d_model=4096, d_expert=1792, E=64, k=8, gelu, fwd+bwd"),
+}
+METRIC = "SMoE MLP fwd+bwd tokens/sec & TFLOPS (% bf16 peak), Mixtral shape, 1/2/4/8 GPU"
+
+
+def flops_per_step(T, d, de, E, k):
+    return 12.0 * T * k * d * de
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port): cpu_baseline and --impl reference
+
+def cpu_oracle_step_time(T, d, de, E, k, seed=0):
+    """One fwd+bwd of the oracle port on T tokens; returns seconds (after one warm call at tiny T)."""
+    import numpy as np
+    from oracle import scattermlp_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (T, d)).astype(np.float32)
+    w1 = (rng.uniform(-1, 1, (E, d, de)) / np.sqrt(d)).astype(np.float32)
+    w2 = (rng.uniform(-1, 1, (E, de, d)) / np.sqrt(de)).astype(np.float32)
+    wg = (rng.uniform(-1, 1, (d, E)) / np.sqrt(d)).astype(np.float32)
+    idx, p = orc.topk_routing(orc.gate_probs(x, wg), k)
+    dy = rng.uniform(-1, 1, (T, d)).astype(np.float32)
+
+    def step():
+        y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, E)
+        orc.smoe_mlp_backward(x, w1, w2, p, st, dy)
+
+    t0 = time.perf_counter()
+    step()
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference's path on the host CPU."""
+    if rank != 0:
+        return
+    T, d, de, E, k, desc = CONFIGS[args.config]
+    sample_t = args.ref_tokens
+    for _ in range(args.warmup):
+        cpu_oracle_step_time(sample_t, d, de, E, k)
+    times = [cpu_oracle_step_time(sample_t, d, de, E, k) for _ in range(args.steps)]
+    total = sum(times)
+    tok_s = sample_t * len(times) / total
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 storage, f64 accumulate",
+        "data": "synthetic",
+        "config": {"workload": desc, "sample_tokens_per_step": sample_t},
+        "tflops": flops_per_step(sample_t, d, de, E, k) * len(times) / total / 1e12,
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"T={sample_t} tokens at {args.config} dims per step (oracle/scattermlp_oracle.py, "
+                                   f"NumPy/OpenBLAS f64 accumulate)"},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_08245_b200 as sm
+    from paper_2403_08245_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    T, d, de, E, k, desc = CONFIGS[args.config]
+    dtype = torch.bfloat16
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = (torch.rand((T, d), generator=g, device=dev) * 2 - 1).to(dtype)
+    dy = (torch.rand((T, d), generator=g, device=dev) * 2 - 1).to(dtype)
+    cfg = sm.SmoeMlpConfig(d_model=d, d_expert=de, num_experts=E, k=k)
+    w1, w2 = sm.init_smoe_mlp_weights(cfg, 101 + rank, dtype=dtype, device=dev, source="device")
+    wg = (torch.rand((d, E), generator=g, device=dev) * 2 - 1) / (d ** 0.5)
+    routing = sm.topk_select(sm.gate_forward(x.float(), wg), k)
+    torch.cuda.synchronize()
+
+    def step(xx, dyy, rt):
+        order = sm.compute_grouped_order(rt)
+        y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
+        grads = sm.smoe_mlp_backward(ctx, dyy)
+        return y, grads
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(x, dy, routing)
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = _lib.launch_count()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        step(x, dy, routing)
+    e1.record(st)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = _lib.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    tokens_total = T * world
+    value = tokens_total / (ms / 1e3)
+    flops = flops_per_step(T, d, de, E, k)
+    peaks, peak_kind = load_peaks()
+    tflops_per_gpu = flops / (ms / 1e3) / 1e12
+
+    # ---- e2e through the public API with pinned host buffers --------------
+    hx = x.cpu().pin_memory()
+    hdy = dy.cpu().pin_memory()
+    hidx = routing.expert_idx.cpu().pin_memory()
+    hp = routing.p.cpu().pin_memory()
+    hdx = torch.empty((T, d), dtype=dtype).pin_memory()
+    hdp = torch.empty((T, k), dtype=torch.float32).pin_memory()
+    h2d = hx.numel() * hx.element_size() + hdy.numel() * hdy.element_size() + hidx.numel() * 8 + hp.numel() * 4
+    d2h = hdx.numel() * hdx.element_size() + hdp.numel() * 4
+
+    def e2e_step():
+        xx = hx.to(dev, non_blocking=True)
+        dyy = hdy.to(dev, non_blocking=True)
+        ids = hidx.to(dev, non_blocking=True)
+        pp = hp.to(dev, non_blocking=True)
+        rt = sm.RoutingResult(expert_idx=ids, p=pp, gate_full=routing.gate_full, renormalized=True, validate=False)
+        _, grads = step(xx, dyy, rt)
+        hdx.copy_(grads.dx, non_blocking=True)
+        hdp.copy_(grads.dp, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t)
+
+    # ---- roofline: dominant kernel (layer-1 forward grouped GEMM) alone ----
+    order = sm.compute_grouped_order(routing)
+    n = T * k
+    h_pre = torch.empty((n, de), dtype=dtype, device=dev)
+    h = torch.empty_like(h_pre)
+    reps = 10
+
+    def l1():
+        sm.scatter2scatter(x, w1, order, k, sm.SCATTERED_TO_GROUPED, out=h_pre, activation="gelu", act_out=h)
+
+    for _ in range(2):
+        l1()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        l1()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_l1 = e0.elapsed_time(e1) / reps
+    l1_flops = 2.0 * n * d * de
+    achieved = l1_flops / (ms_l1 / 1e3) / 1e12
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(f"{args.config}:{sm.get_engine()}:l1_fwd")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "kernel": "scatter2scatter S->G layer-1 fwd (gather + grouped GEMM + fused GELU epilogue)",
+                "algorithmic": f"2*T*k*d_model*d_expert = {l1_flops:.4g} FLOP per launch",
+                "ms_per_launch": ms_l1, "peak_kind": f"{peak_kind} burst (kernel timed alone)"}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample_t = args.ref_tokens
+        secs = cpu_oracle_step_time(sample_t, d, de, E, k)
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        cpu_baseline = {"value": sample_t / secs, "unit": "tokens/s", "cores": cores, "kind": "port",
+                        "sample": f"one fwd+bwd of T={sample_t} tokens at {args.config} dims "
+                                  f"(oracle/scattermlp_oracle.py, NumPy/OpenBLAS, f64 accumulate), {secs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, softmax top-k routing)",
+            "config": {"workload": desc, "global_batch": T * world, "seq_len": None,
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (W1+W2 1.9 GB, H 1.9 GB); no flush",
+                       "engine": sm.get_engine(), "timed": "flatten_and_sort + smoe_mlp_forward + smoe_mlp_backward"},
+            "tflops_per_gpu": tflops_per_gpu,
+            "pct_bf16_peak": tflops_per_gpu / peaks["bf16_tflops"],
+            "pct_bf16_peak_sustained": tflops_per_gpu / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+            "e2e": {"value": tokens_total / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu_baseline,
+            "clocks": clocks,
+            "peak_memory_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-tokens", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if args.ref_tokens == 128:
+            args.ref_tokens = 64
+        run_reference(args, rank, world)
+        return
+
+    if args.engine:
+        import paper_2403_08245_b200 as sm
+        sm.set_engine(args.engine)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

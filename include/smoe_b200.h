@@ -1,0 +1,153 @@
+/*
+ * smoe_b200.h — C ABI of libsmoe_b200.so, the B200 (sm_100a) implementation of
+ * the ScatterMoE ParallelLinear hot path.
+ *
+ * Each entry point replaces one function of the reference package
+ * `scattermlp` (/root/reference/pkg/src/scattermlp); the reference interface it
+ * stands in for is cited above each declaration.  The reference is an
+ * in-process Python/NumPy API, so the "FFI" a maintainer would bind is a
+ * ctypes shim; the Python package
+ * `paper_2403_08245_b200` is exactly that shim plus the reference's host logic.
+ *
+ * Conventions (all functions):
+ *   - every pointer is a DEVICE pointer unless stated otherwise;
+ *   - the library never allocates device memory: the caller passes every
+ *     output and workspace buffer (reference `out=` discipline,
+ *     kernels.py:186-197, parallel_linear.py:144-154);
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*) and is
+ *     asynchronous; no call synchronises the host, so every call is CUDA-graph
+ *     capturable;
+ *   - sizes are int64; index tensors (orders, offsets, inverse) are int32
+ *     (n = T*k < 2^31);
+ *   - rows are dense row-major with the stated column count as the row stride;
+ *   - return value is an smoe_status; on failure smoe_get_last_error() returns
+ *     a thread-local message naming the offending argument / shapes.
+ */
+#ifndef SMOE_B200_H
+#define SMOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMOE_ABI_VERSION 1
+
+typedef enum {
+  SMOE_OK = 0,
+  SMOE_EINVAL = 1,  /* bad argument value  (reference: ValueError)            */
+  SMOE_ESHAPE = 2,  /* shape mismatch      (reference: DimensionError, errors.py:12-19) */
+  SMOE_ECUDA = 3,   /* CUDA launch / runtime failure                         */
+  SMOE_ENOTSUP = 4  /* valid but unsupported combination on this build        */
+} smoe_status;
+
+typedef enum { SMOE_F32 = 0, SMOE_BF16 = 1 } smoe_dtype;
+
+/* Activations of moe_layers.py:42-72 (exact-erf GELU, ReLU, SiLU). */
+typedef enum { SMOE_ACT_GELU = 0, SMOE_ACT_RELU = 1, SMOE_ACT_SILU = 2 } smoe_activation;
+
+/* scatter2scatter epilogues (fusions of moe_layers.py:169-175 and :205-206). */
+typedef enum {
+  SMOE_EPI_NONE = 0,     /* out[dst] = acc                                          */
+  SMOE_EPI_ACT = 1,      /* out[dst] = pre = acc;  out2[dst] = act(pre)             */
+  SMOE_EPI_ACT_GRAD = 2, /* out[dst] = acc * act'(aux[dst])   (aux = h_pre)         */
+  SMOE_EPI_ACT_ONLY = 3  /* out[dst] = act(acc)  (inference: no pre-activation kept)  */
+} smoe_epilogue;
+
+/* GEMM engine selection: AUTO picks tcgen05 for bf16 and the SIMT fp32 kernel
+ * for the fp32 check mode. */
+typedef enum { SMOE_ENGINE_AUTO = 0, SMOE_ENGINE_SIMT = 1, SMOE_ENGINE_TCGEN05 = 2 } smoe_engine;
+
+const char *smoe_get_last_error(void);
+int smoe_abi_version(void);
+/* Number of kernels this library has enqueued since load (all threads). */
+uint64_t smoe_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Routing: replaces router.compute_grouped_order (router.py:154-164) and
+ * GroupedOrder.inverse (router.py:112-116); north_star name flatten_and_sort.
+ *   expert_idx            [n] int64 (the T x k routing ids, token-major)
+ *   sorted_scattered_idxs [n] int32 (GroupedOrder.o: stable argsort)
+ *   sorted_expert_idxs    [n] int32 (expert id at each grouped position)
+ *   expert_offsets        [E+1] int32 (GroupedOrder.bin_offsets)
+ *   inverse               [n] int32 or NULL (scattered slot -> grouped pos)
+ * Returns SMOE_EINVAL (no device check) when ids fall outside [0,E) — ids are
+ * validated on the host side of the shim, as RoutingResult.__post_init__ does.
+ */
+size_t smoe_route_sort_workspace_bytes(int64_t n, int32_t num_experts);
+int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
+                    int32_t *sorted_scattered_idxs, int32_t *sorted_expert_idxs,
+                    int32_t *expert_offsets, int32_t *inverse, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * scatter2scatter (kernels.py:143-220): for each grouped position i in bin e,
+ *   src = grouped_in ? i : order[i] / fan_out
+ *   dst = grouped_out ? i : order[i]
+ *   out[dst] = x[src] @ (transpose_w ? W[e]^T : W[e])   (+ epilogue)
+ *   x        [x_rows, d_in]           x_rows = n (grouped_in) or n / fan_out
+ *   w        [E, w_rows, w_cols]      d_in,d_out = (w_rows,w_cols) or swapped
+ *   out/out2 [n, d_out]               aux [n, d_out] (EPI_ACT_GRAD only)
+ * dtype applies to x, w, out, out2, aux.  Accumulation is fp32.
+ */
+int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                         int64_t w_rows, int64_t w_cols, const int32_t *order,
+                         const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                         int32_t grouped_in, int32_t grouped_out, int32_t transpose_w,
+                         int32_t dtype, int32_t epilogue, int32_t activation, void *out,
+                         void *out2, const void *aux, int32_t engine, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * group_xty (kernels.py:329-361): dw[e] = xg[bin e]^T @ yg[bin e]; empty bin -> 0.
+ *   xg [n, d_in], yg [n, d_out] (grouped order), dw [E, d_in, d_out]
+ */
+int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets,
+                   int32_t num_experts, int64_t n, int64_t d_in, int64_t d_out,
+                   int32_t dtype, void *dw, int32_t engine, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * group (kernels.py:289-326): out[i] = x[order[i] / fan_out] * (weights ? weights[order[i]] : 1)
+ *   x [n / fan_out, d], weights [n] float32 or NULL, out [n, d]
+ */
+int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, int64_t n,
+               int32_t fan_out, const float *weights, int32_t dtype, void *out, void *stream);
+
+/* _combine (parallel_linear.py:69-73): y[s] = sum_j p[s,j] * y_hat[s*J + j]
+ *   y_hat [S*J, d], p [S, J] float32, y [S, d]                            */
+int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_cols, int64_t d,
+                 int32_t dtype, void *y, void *stream);
+
+/* dp (parallel_linear.py:198-206): dp[s,j] = <dy[s], y_hat[s*J + j]>
+ *   dy [S, d], y_hat [S*J, d], dp [S, J] float32                          */
+int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
+                        int64_t d, int32_t dtype, float *dp, void *stream);
+
+/* fan-out reduce (parallel_linear.py:259-266): dx[t] = sum_j g[t*F + j]
+ *   g [T*F, d], dx [T, d]                                                 */
+int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, int64_t d,
+                       int32_t dtype, void *dx, void *stream);
+
+/* elementwise activation / derivative (moe_layers.py:75-83), rounded once.
+ *   apply: out = act(x);  grad: out = act'(x)                            */
+int smoe_apply_activation(const void *x, int64_t numel, int32_t activation, int32_t derivative,
+                    int32_t dtype, void *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * scatter_combine (kernels.py:242-286), inference: y[order[i] / combine_cols] +=
+ *   p_flat[order[i]] * (x[src] @ W[e]) with no T*k buffer.
+ *   y_accum [n / combine_cols, d_out] float32, zeroed by this call.
+ *   y       [n / combine_cols, d_out] dtype (rounded copy of y_accum; may be
+ *           the same buffer as y_accum when dtype == SMOE_F32).
+ */
+int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                         int64_t d_in, int64_t d_out, const int32_t *order,
+                         const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                         const float *p_flat, int32_t combine_cols, int32_t grouped_in,
+                         int32_t dtype, float *y_accum, void *y, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMOE_B200_H */

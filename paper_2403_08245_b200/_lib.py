@@ -1,0 +1,97 @@
+"""ctypes binding of libsmoe_b200.so (the C ABI declared in include/smoe_b200.h).
+
+This is the FFI a maintainer of the reference would add: the reference is an
+in-process NumPy package, so its "plugin boundary" is a Python call; the shim
+here hands device pointers, sizes and the current CUDA stream to the C ABI.
+
+There is deliberately no fallback: if the shared library is missing or fails
+to load, every product entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libsmoe_b200.so"
+
+SMOE_OK, SMOE_EINVAL, SMOE_ESHAPE, SMOE_ECUDA, SMOE_ENOTSUP = range(5)
+SMOE_F32, SMOE_BF16 = 0, 1
+ACTIVATION_IDS = {"gelu": 0, "relu": 1, "silu": 2}
+EPI_NONE, EPI_ACT, EPI_ACT_GRAD, EPI_ACT_ONLY = 0, 1, 2, 3
+ENGINE_IDS = {"auto": 0, "simt": 1, "tcgen05": 2}
+
+_c = ctypes
+_vp, _i64, _i32, _sz = _c.c_void_p, _c.c_int64, _c.c_int32, _c.c_size_t
+
+# name -> (restype, argtypes); the exact signatures of include/smoe_b200.h
+SIGNATURES = {
+    "smoe_get_last_error": (_c.c_char_p, []),
+    "smoe_abi_version": (_c.c_int, []),
+    "smoe_launch_count": (_c.c_uint64, []),
+    "smoe_route_sort_workspace_bytes": (_sz, [_i64, _i32]),
+    "smoe_route_sort": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "smoe_scatter2scatter": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
+                                        _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_group_xty": (_c.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i32, _vp]),
+    "smoe_group": (_c.c_int, [_vp, _i64, _i64, _vp, _i64, _i32, _vp, _i32, _vp, _vp]),
+    "smoe_combine": (_c.c_int, [_vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
+    "smoe_combine_grad_p": (_c.c_int, [_vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
+    "smoe_fanout_reduce": (_c.c_int, [_vp, _i64, _i32, _i64, _i32, _vp, _vp]),
+    "smoe_apply_activation": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_scatter_combine": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
+                                        _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+}
+
+_lib = None
+_load_error: str | None = None
+
+
+class LibraryError(RuntimeError):
+    """The native library is missing or a native call failed."""
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes handle; raises if unavailable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        _load_error = f"{p} not found; run `python -m paper_2403_08245_b200.build` (no CPU fallback exists)"
+        raise LibraryError(_load_error)
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.smoe_abi_version() != 1:
+        raise LibraryError("libsmoe_b200.so ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def launch_count() -> int:
+    """Kernels enqueued by libsmoe_b200.so since load (evidence for gpu_launches)."""
+    return int(load().smoe_launch_count())
+
+
+def last_error() -> str:
+    return load().smoe_get_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str) -> None:
+    """Map a C status onto the reference's exception classes (errors.py:3-19)."""
+    if status == SMOE_OK:
+        return
+    from .errors import DimensionError
+
+    msg = f"{what}: {last_error()}"
+    if status == SMOE_ESHAPE:
+        raise DimensionError(msg)
+    if status == SMOE_EINVAL:
+        raise ValueError(msg)
+    if status == SMOE_ENOTSUP:
+        raise NotImplementedError(msg)
+    raise LibraryError(msg)

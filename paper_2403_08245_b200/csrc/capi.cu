@@ -1,0 +1,189 @@
+// extern "C" entry points of libsmoe_b200.so (declared in include/smoe_b200.h).
+// Argument validation mirrors the reference's checks so the Python shim can map
+// status codes back onto the same exception classes (errors.py:3-19).
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace smoe {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int status, const std::string &msg) {
+  set_error(msg);
+  return status;
+}
+int check_launch(const char *what, int launches) {
+  g_launches.fetch_add((uint64_t)launches, std::memory_order_relaxed);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(SMOE_ECUDA, std::string(what) + ": " + cudaGetErrorString(err));
+  return SMOE_OK;
+}
+
+// engines (defined in the other translation units)
+size_t route_sort_workspace(int64_t n, int E);
+int route_sort(const int64_t *, int64_t, int, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
+int group(const void *, int64_t, const int32_t *, int64_t, int, const float *, int, void *, cudaStream_t);
+int combine(const void *, const float *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, float *, cudaStream_t);
+int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int activation(const void *, int64_t, int, int, int, void *, cudaStream_t);
+int simt_scatter2scatter(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
+int simt_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int, void *, cudaStream_t);
+int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, const float *, int, int, int, float *, void *, cudaStream_t);
+bool tc_available();
+int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
+int tc_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+
+}  // namespace smoe
+
+using namespace smoe;
+
+#define REQUIRE(cond, status, msg)          \
+  do {                                      \
+    if (!(cond)) return fail(status, msg);  \
+  } while (0)
+
+static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline std::string dims(int64_t a, int64_t b) {
+  return "(" + std::to_string(a) + ", " + std::to_string(b) + ")";
+}
+static inline bool valid_dtype(int32_t d) { return d == SMOE_F32 || d == SMOE_BF16; }
+
+extern "C" {
+
+const char *smoe_get_last_error(void) { return g_last_error.c_str(); }
+int smoe_abi_version(void) { return SMOE_ABI_VERSION; }
+uint64_t smoe_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+size_t smoe_route_sort_workspace_bytes(int64_t n, int32_t num_experts) {
+  return route_sort_workspace(n, num_experts);
+}
+
+int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
+                    int32_t *sorted_scattered_idxs, int32_t *sorted_expert_idxs,
+                    int32_t *expert_offsets, int32_t *inverse, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+  REQUIRE(n == 0 || (expert_idx && sorted_scattered_idxs), SMOE_EINVAL, "route_sort: null pointer");
+  REQUIRE(expert_offsets, SMOE_EINVAL, "route_sort: null expert_offsets");
+  return route_sort(expert_idx, n, num_experts, sorted_scattered_idxs, sorted_expert_idxs,
+                    expert_offsets, inverse, workspace, workspace_bytes, S(stream));
+}
+
+int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                         int64_t w_rows, int64_t w_cols, const int32_t *order,
+                         const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                         int32_t grouped_in, int32_t grouped_out, int32_t transpose_w,
+                         int32_t dtype, int32_t epilogue, int32_t activation, void *out,
+                         void *out2, const void *aux, int32_t engine, void *stream) {
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1, got " + std::to_string(fan_out));
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype " + std::to_string(dtype));
+  REQUIRE(num_experts >= 1, SMOE_EINVAL, "num_experts must be >= 1");
+  REQUIRE(epilogue >= SMOE_EPI_NONE && epilogue <= SMOE_EPI_ACT_ONLY, SMOE_EINVAL, "bad epilogue");
+  REQUIRE(activation >= SMOE_ACT_GELU && activation <= SMOE_ACT_SILU, SMOE_EINVAL, "bad activation");
+  if (grouped_in)
+    REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots: " + dims(x_rows, 0) + " vs " + dims(n, 0));
+  else
+    REQUIRE(x_rows * fan_out == n, SMOE_EINVAL,
+            "scattered input rows (" + std::to_string(x_rows) + ") * fan_out (" + std::to_string(fan_out) +
+                ") must equal T*k (" + std::to_string(n) + ")");
+  REQUIRE(epilogue != SMOE_EPI_ACT || out2, SMOE_EINVAL, "EPI_ACT needs out2");
+  REQUIRE(epilogue != SMOE_EPI_ACT_GRAD || aux, SMOE_EINVAL, "EPI_ACT_GRAD needs aux");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(x && w && order && expert_offsets && out, SMOE_EINVAL, "scatter2scatter: null pointer");
+  bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available());
+  if (use_tc) {
+    REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
+    return tc_scatter2scatter(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
+                              grouped_in, grouped_out, transpose_w, epilogue, activation, out, out2, aux, S(stream));
+  }
+  return simt_scatter2scatter(x, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out, grouped_in,
+                              grouped_out, transpose_w, dtype, epilogue, activation, out, out2, aux, S(stream));
+}
+
+int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets,
+                   int32_t num_experts, int64_t n, int64_t d_in, int64_t d_out, int32_t dtype,
+                   void *dw, int32_t engine, void *stream) {
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype " + std::to_string(dtype));
+  REQUIRE(num_experts >= 1, SMOE_EINVAL, "num_experts must be >= 1");
+  REQUIRE(dw && expert_offsets, SMOE_EINVAL, "group_xty: null pointer");
+  REQUIRE(n == 0 || (xg && yg), SMOE_EINVAL, "group_xty: null pointer");
+  bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available());
+  if (use_tc) {
+    REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only");
+    return tc_group_xty(xg, yg, expert_offsets, num_experts, n, d_in, d_out, dw, S(stream));
+  }
+  return simt_group_xty(xg, yg, expert_offsets, num_experts, d_in, d_out, dtype, dw, S(stream));
+}
+
+int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, int64_t n,
+               int32_t fan_out, const float *weights, int32_t dtype, void *out, void *stream) {
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1, got " + std::to_string(fan_out));
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  REQUIRE(x_rows * fan_out == n, SMOE_EINVAL,
+          "input rows (" + std::to_string(x_rows) + ") * fan_out (" + std::to_string(fan_out) +
+              ") must equal T*k (" + std::to_string(n) + ")");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(x && order && out, SMOE_EINVAL, "group: null pointer");
+  return group(x, d, order, n, fan_out, weights, dtype, out, S(stream));
+}
+
+int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_cols, int64_t d,
+                 int32_t dtype, void *y, void *stream) {
+  REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine: J must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (s_rows == 0) return SMOE_OK;
+  REQUIRE(y_hat && p && y, SMOE_EINVAL, "combine: null pointer");
+  return combine(y_hat, p, s_rows, j_cols, d, dtype, y, S(stream));
+}
+
+int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
+                        int64_t d, int32_t dtype, float *dp, void *stream) {
+  REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine_grad_p: J must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (s_rows == 0) return SMOE_OK;
+  REQUIRE(dy && y_hat && dp, SMOE_EINVAL, "combine_grad_p: null pointer");
+  return combine_grad_p(dy, y_hat, s_rows, j_cols, d, dtype, dp, S(stream));
+}
+
+int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, int64_t d,
+                       int32_t dtype, void *dx, void *stream) {
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (t_rows == 0) return SMOE_OK;
+  REQUIRE(slot_grads && dx, SMOE_EINVAL, "fanout_reduce: null pointer");
+  return fanout_reduce(slot_grads, t_rows, fan_out, d, dtype, dx, S(stream));
+}
+
+int smoe_apply_activation(const void *x, int64_t numel, int32_t act, int32_t derivative, int32_t dtype,
+                    void *out, void *stream) {
+  REQUIRE(act >= SMOE_ACT_GELU && act <= SMOE_ACT_SILU, SMOE_EINVAL, "bad activation");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (numel == 0) return SMOE_OK;
+  REQUIRE(x && out, SMOE_EINVAL, "activation: null pointer");
+  return activation(x, numel, act, derivative, dtype, out, S(stream));
+}
+
+int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                         int64_t d_in, int64_t d_out, const int32_t *order,
+                         const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                         const float *p_flat, int32_t combine_cols, int32_t grouped_in,
+                         int32_t dtype, float *y_accum, void *y, void *stream) {
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
+  REQUIRE(combine_cols >= 1 && n % combine_cols == 0, SMOE_EINVAL,
+          "combine width " + std::to_string(combine_cols) + " must divide T*k (" + std::to_string(n) + ")");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (grouped_in)
+    REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");
+  else
+    REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
+  REQUIRE(y_accum && y, SMOE_EINVAL, "scatter_combine: null output");
+  return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n, fan_out, p_flat,
+                              combine_cols, grouped_in, dtype, y_accum, y, S(stream));
+}
+
+}  // extern "C"

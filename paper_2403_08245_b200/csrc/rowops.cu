@@ -1,0 +1,273 @@
+// HBM-bound row kernels of the ParallelLinear path (K5/K9 and the combine /
+// fan-out reductions of SURVEY.md §2.3).  One warp owns one output row and
+// moves it with 16-byte vectors; all sums are fp32 and written once, so the
+// results are deterministic (no atomics anywhere).
+//
+//   group            kernels.py:289-326       out[i] = x[o[i]/F] * w[o[i]]
+//   combine          parallel_linear.py:69-73 y[s]  = sum_j p[s,j] y_hat[s*J+j]
+//   combine_grad_p   parallel_linear.py:198-206  dp[s,j] = <dy[s], y_hat[s*J+j]>
+//   fanout_reduce    parallel_linear.py:259-266  dx[t] = sum_j g[t*F+j]
+//   activation       moe_layers.py:75-83      act(x) / act'(x)
+#include "common.cuh"
+
+namespace smoe {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+
+template <typename T> struct alignas(16) Vec {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+
+template <typename T> __device__ __forceinline__ Vec<T> ldv(const T *p) {
+  Vec<T> r;
+  *reinterpret_cast<uint4 *>(&r) = __ldg(reinterpret_cast<const uint4 *>(p));
+  return r;
+}
+template <typename T> __device__ __forceinline__ void stv(T *p, const Vec<T> &v) {
+  *reinterpret_cast<uint4 *>(p) = *reinterpret_cast<const uint4 *>(&v);
+}
+
+static inline bool vec_ok(const void *p, int64_t d, size_t esz) {
+  return ((uintptr_t)p % 16 == 0) && ((d * (int64_t)esz) % 16 == 0);
+}
+
+// ---- group -----------------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict__ x, int64_t d,
+                                                             const int32_t *__restrict__ order,
+                                                             int64_t n, int fan_out,
+                                                             const float *__restrict__ weights,
+                                                             T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int32_t slot = order[i];
+  const T *src = x + (int64_t)(slot / fan_out) * d;
+  T *dst = out + i * d;
+  const float wgt = weights ? weights[slot] : 1.0f;
+  if (VEC) {
+    constexpr int N = Vec<T>::N;
+    for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+      Vec<T> v = ldv(src + c);
+      if (weights) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) v.v[q] = Num<T>::from_f(Num<T>::to_f(v.v[q]) * wgt);
+      }
+      stv(dst + c, v);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      T v = src[c];
+      dst[c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt) : v;
+    }
+  }
+}
+
+// ---- combine ---------------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,
+                                                               const float *__restrict__ p,
+                                                               int64_t S, int J, int64_t d,
+                                                               T *__restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (s >= S) return;
+  const T *src = y_hat + s * J * d;
+  T *dst = y + s * d;
+  if (VEC) {
+    constexpr int N = Vec<T>::N;
+    for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+      float acc[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) acc[q] = 0.f;
+      for (int j = 0; j < J; ++j) {
+        const float pj = p[s * J + j];
+        Vec<T> v = ldv(src + (int64_t)j * d + c);
+#pragma unroll
+        for (int q = 0; q < N; ++q) acc[q] = fmaf(pj, Num<T>::to_f(v.v[q]), acc[q]);
+      }
+      Vec<T> o;
+#pragma unroll
+      for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(acc[q]);
+      stv(dst + c, o);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      float acc = 0.f;
+      for (int j = 0; j < J; ++j) acc = fmaf(p[s * J + j], Num<T>::to_f(src[(int64_t)j * d + c]), acc);
+      dst[c] = Num<T>::from_f(acc);
+    }
+  }
+}
+
+// ---- dp --------------------------------------------------------------------
+// One warp per combine row s; J partial dot products reduced with shuffles.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kRowThreads) combine_grad_p_kernel(const T *__restrict__ dy,
+                                                                      const T *__restrict__ y_hat,
+                                                                      int64_t S, int J, int64_t d,
+                                                                      float *__restrict__ dp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (s >= S) return;
+  const T *g = dy + s * d;
+  for (int j = 0; j < J; ++j) {
+    const T *yh = y_hat + (s * J + j) * d;
+    float acc = 0.f;
+    if (VEC) {
+      constexpr int N = Vec<T>::N;
+      for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+        Vec<T> a = ldv(g + c), b = ldv(yh + c);
+#pragma unroll
+        for (int q = 0; q < N; ++q) acc = fmaf(Num<T>::to_f(a.v[q]), Num<T>::to_f(b.v[q]), acc);
+      }
+    } else {
+      for (int64_t c = lane; c < d; c += 32) acc = fmaf(Num<T>::to_f(g[c]), Num<T>::to_f(yh[c]), acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dp[s * J + j] = acc;
+  }
+}
+
+// ---- fan-out reduce --------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__restrict__ g,
+                                                                     int64_t Trows, int F,
+                                                                     int64_t d,
+                                                                     T *__restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (t >= Trows) return;
+  const T *src = g + t * F * d;
+  T *dst = dx + t * d;
+  if (VEC) {
+    constexpr int N = Vec<T>::N;
+    for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+      float acc[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) acc[q] = 0.f;
+      for (int j = 0; j < F; ++j) {
+        Vec<T> v = ldv(src + (int64_t)j * d + c);
+#pragma unroll
+        for (int q = 0; q < N; ++q) acc[q] += Num<T>::to_f(v.v[q]);
+      }
+      Vec<T> o;
+#pragma unroll
+      for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(acc[q]);
+      stv(dst + c, o);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      float acc = 0.f;
+      for (int j = 0; j < F; ++j) acc += Num<T>::to_f(src[(int64_t)j * d + c]);
+      dst[c] = Num<T>::from_f(acc);
+    }
+  }
+}
+
+// ---- activation ------------------------------------------------------------
+template <typename T>
+__global__ void activation_kernel(const T *__restrict__ x, int64_t numel, int act, int deriv,
+                                  T *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float z = Num<T>::to_f(x[i]);
+    out[i] = Num<T>::from_f(deriv ? act_grad(act, z) : act_fwd(act, z));
+  }
+}
+
+// ---- dispatch --------------------------------------------------------------
+static inline unsigned row_blocks(int64_t rows) { return (unsigned)((rows + kRowWarps - 1) / kRowWarps); }
+
+int group(const void *x, int64_t d, const int32_t *order, int64_t n, int fan_out,
+          const float *w, int dtype, void *out, cudaStream_t st) {
+  if (n == 0 || d == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    if (vec_ok(x, d, 2) && vec_ok(out, d, 2))
+      group_kernel<T, true><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
+    else
+      group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
+  } else {
+    using T = float;
+    if (vec_ok(x, d, 4) && vec_ok(out, d, 4))
+      group_kernel<T, true><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
+    else
+      group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
+  }
+  return check_launch("group");
+}
+
+int combine(const void *y_hat, const float *p, int64_t S, int J, int64_t d, int dtype, void *y,
+            cudaStream_t st) {
+  if (S == 0 || d == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    if (vec_ok(y_hat, d, 2) && vec_ok(y, d, 2))
+      combine_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+    else
+      combine_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+  } else {
+    using T = float;
+    if (vec_ok(y_hat, d, 4) && vec_ok(y, d, 4))
+      combine_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+    else
+      combine_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+  }
+  return check_launch("combine");
+}
+
+int combine_grad_p(const void *dy, const void *y_hat, int64_t S, int J, int64_t d, int dtype,
+                   float *dp, cudaStream_t st) {
+  if (S == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    if (vec_ok(dy, d, 2) && vec_ok(y_hat, d, 2))
+      combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
+    else
+      combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
+  } else {
+    using T = float;
+    if (vec_ok(dy, d, 4) && vec_ok(y_hat, d, 4))
+      combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
+    else
+      combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
+  }
+  return check_launch("combine_grad_p");
+}
+
+int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx,
+                  cudaStream_t st) {
+  if (Trows == 0 || d == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    if (vec_ok(g, d, 2) && vec_ok(dx, d, 2))
+      fanout_reduce_kernel<T, true><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+    else
+      fanout_reduce_kernel<T, false><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+  } else {
+    using T = float;
+    if (vec_ok(g, d, 4) && vec_ok(dx, d, 4))
+      fanout_reduce_kernel<T, true><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+    else
+      fanout_reduce_kernel<T, false><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+  }
+  return check_launch("fanout_reduce");
+}
+
+int activation(const void *x, int64_t numel, int act, int deriv, int dtype, void *out,
+               cudaStream_t st) {
+  if (numel == 0) return SMOE_OK;
+  int64_t blocks64 = (numel + 255) / 256;
+  unsigned blocks = (unsigned)(blocks64 < 148 * 32 ? blocks64 : 148 * 32);
+  if (dtype == SMOE_BF16)
+    activation_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16 *)x, numel, act, deriv, (__nv_bfloat16 *)out);
+  else
+    activation_kernel<float><<<blocks, 256, 0, st>>>((const float *)x, numel, act, deriv, (float *)out);
+  return check_launch("activation");
+}
+
+}  // namespace smoe

@@ -1,0 +1,377 @@
+"""Padding-free grouped kernels over scattered or grouped row layouts (GPU).
+
+Same API as the reference kernels.py (/root/reference/pkg/src/scattermlp/kernels.py):
+scatter2scatter (:143-220), scatter_combine (:242-286), group (:289-326),
+group_xty (:329-361), LayoutFlag + the four layout constants (:61-72),
+TileConfig (:46-58), the MAC counter (:74-98) and the fault hook (:100-107).
+
+Arguments are torch CUDA tensors: activations (rows, cols) in bfloat16 or
+float32, expert stacks (E, d_in, d_out) of the same dtype, combine weights in
+float32.  Every call enqueues sm_100a kernels from libsmoe_b200.so on the
+current stream; nothing here computes on the CPU and there is no fallback.
+
+TileConfig is accepted for API compatibility and ignored: the GPU kernels
+choose their own tiles, and results never depend on tiling (the reference's
+own invariant, kernels.py:46-49).
+"""
+from __future__ import annotations
+
+import os
+import threading
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .errors import require_dims
+from .router import GroupedOrder
+
+
+def default_worker_count() -> int:
+    env = os.environ.get("SCATTERMLP_WORKERS")
+    if env is not None:
+        n = int(env)
+        if n < 1:
+            raise ValueError(f"SCATTERMLP_WORKERS must be >= 1, got {n}")
+        return n
+    return os.cpu_count() or 1
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Reference blocking knobs (kernels.py:46-58); accepted, validated, unused on GPU."""
+
+    tile_rows: int = 64
+    tile_cols: int = 64
+    tile_inner: int = 64
+    worker_count: int = field(default_factory=default_worker_count)
+
+    def __post_init__(self):
+        for name in ("tile_rows", "tile_cols", "tile_inner", "worker_count"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be >= 1, got {getattr(self, name)}")
+
+
+@dataclass(frozen=True)
+class LayoutFlag:
+    """Whether the kernel's input/output rows are in grouped (bin) order."""
+
+    grouped_in: bool = False
+    grouped_out: bool = False
+
+
+SCATTERED_TO_GROUPED = LayoutFlag(grouped_in=False, grouped_out=True)
+GROUPED_TO_SCATTERED = LayoutFlag(grouped_in=True, grouped_out=False)
+SCATTERED_TO_SCATTERED = LayoutFlag(grouped_in=False, grouped_out=False)
+GROUPED_TO_GROUPED = LayoutFlag(grouped_in=True, grouped_out=True)
+
+# ---- analytic MAC counter (kernels.py:74-98) and fault hook (:100-107) -------
+_mac_lock = threading.Lock()
+_mac_count = 0
+_fault_inject = False
+_engine = os.environ.get("SMOE_ENGINE", "auto")
+
+
+def reset_mac_count() -> None:
+    global _mac_count
+    with _mac_lock:
+        _mac_count = 0
+
+
+def mac_count() -> int:
+    with _mac_lock:
+        return _mac_count
+
+
+def add_macs(n: int) -> None:
+    global _mac_count
+    with _mac_lock:
+        _mac_count += int(n)
+
+
+def _credit(order: GroupedOrder, d_in: int, d_out: int) -> None:
+    # sum_e count_e * d_in * d_out == num_slots * d_in * d_out: padding-free.
+    add_macs(order.num_slots * d_in * d_out)
+
+
+def set_fault_injection(enabled: bool) -> None:
+    """Test hook: corrupt one scatter2scatter output element per call."""
+    global _fault_inject
+    _fault_inject = bool(enabled)
+
+
+def set_engine(name: str) -> None:
+    """Select the GEMM engine: 'auto' (tcgen05 for bf16, SIMT for fp32), 'simt', 'tcgen05'."""
+    global _engine
+    if name not in _lib.ENGINE_IDS:
+        raise ValueError(f"unknown engine {name!r}; choose from {sorted(_lib.ENGINE_IDS)}")
+    _engine = name
+
+
+def get_engine() -> str:
+    return _engine
+
+
+# ---- helpers -------------------------------------------------------------------
+
+def _dtype_id(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.SMOE_BF16
+    if t.dtype == torch.float32:
+        return _lib.SMOE_F32
+    raise ValueError(f"unsupported element type {t.dtype}; use bfloat16 or float32")
+
+
+def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    return t if t.is_contiguous() else t.contiguous()
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _engine_id(engine: str | None) -> int:
+    return _lib.ENGINE_IDS[engine or _engine]
+
+
+# ---- kernels ---------------------------------------------------------------------
+
+def scatter2scatter(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    order: GroupedOrder,
+    fan_out: int,
+    layout: LayoutFlag = SCATTERED_TO_SCATTERED,
+    tile: TileConfig | None = None,
+    *,
+    transpose_w: bool = False,
+    out: torch.Tensor | None = None,
+    activation: str | None = None,
+    act_out: torch.Tensor | None = None,
+    act_grad_of: torch.Tensor | None = None,
+    engine: str | None = None,
+) -> torch.Tensor:
+    """Fused gather -> per-expert linear transform -> scatter (kernels.py:143-220).
+
+    Returns a T*k x d_out tensor in grouped order when layout.grouped_out else
+    in scattered slot order.  Extensions beyond the reference (fused epilogues):
+      activation + act_out: out holds the pre-activation, act_out = act(out)
+        (the fusion of moe_layers.py:169-175);
+      activation + act_grad_of: out = (x @ W) * act'(act_grad_of)  (moe_layers.py:205-206);
+      activation alone: out = act(x @ W)  (inference, no pre-activation kept).
+    """
+    if fan_out < 1:
+        raise ValueError(f"fan_out must be >= 1, got {fan_out}")
+    num_slots = order.num_slots
+    if w.dim() != 3:
+        raise ValueError(f"expected a 3-D expert stack, got shape {tuple(w.shape)}")
+    require_dims(order.num_experts == w.shape[0], "order bins vs expert stack",
+                 (order.num_experts,), (w.shape[0],))
+    d_in = w.shape[2] if transpose_w else w.shape[1]
+    d_out = w.shape[1] if transpose_w else w.shape[2]
+    require_dims(x.shape[1] == d_in, "input width vs expert weights", tuple(x.shape), (d_in, d_out))
+    if layout.grouped_in:
+        require_dims(x.shape[0] == num_slots, "grouped input rows vs slots", (x.shape[0],), (num_slots,))
+    elif x.shape[0] * fan_out != num_slots:
+        raise ValueError(
+            f"scattered input rows ({x.shape[0]}) * fan_out ({fan_out}) must equal T*k ({num_slots})")
+    if w.dtype != x.dtype:
+        raise ValueError(f"weight dtype {w.dtype} does not match input dtype {x.dtype}")
+    if out is not None:
+        require_dims(tuple(out.shape) == (num_slots, d_out), "out buffer", tuple(out.shape), (num_slots, d_out))
+        if out.dtype != x.dtype:
+            raise ValueError(f"out dtype {out.dtype} does not match input dtype {x.dtype}")
+        if not out.is_contiguous():
+            raise ValueError("out buffer must be contiguous")
+    x = _cuda(x, "x")
+    w = _cuda(w, "w")
+    if out is None:
+        out = torch.empty((num_slots, d_out), dtype=x.dtype, device=x.device)
+    epi, act_id, aux = _lib.EPI_NONE, 0, None
+    if activation is not None:
+        if activation not in _lib.ACTIVATION_IDS:
+            raise ValueError(f"unknown activation {activation!r}; choose from {sorted(_lib.ACTIVATION_IDS)}")
+        act_id = _lib.ACTIVATION_IDS[activation]
+        if act_out is not None and act_grad_of is not None:
+            raise ValueError("activation takes at most one of act_out / act_grad_of")
+        if act_out is None and act_grad_of is None:
+            epi = _lib.EPI_ACT_ONLY
+        elif act_out is not None:
+            epi = _lib.EPI_ACT
+            require_dims(tuple(act_out.shape) == (num_slots, d_out), "act_out buffer",
+                         tuple(act_out.shape), (num_slots, d_out))
+        else:
+            epi = _lib.EPI_ACT_GRAD
+            require_dims(tuple(act_grad_of.shape) == (num_slots, d_out), "act_grad_of",
+                         tuple(act_grad_of.shape), (num_slots, d_out))
+            aux = _cuda(act_grad_of, "act_grad_of")
+    lib = _lib.load()
+    st = lib.smoe_scatter2scatter(
+        x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], w.shape[1], w.shape[2],
+        order.o.data_ptr(), order.bin_offsets.data_ptr(), num_slots, fan_out,
+        int(layout.grouped_in), int(layout.grouped_out), int(transpose_w), _dtype_id(x), epi, act_id,
+        out.data_ptr(), _ptr(act_out), _ptr(aux), _engine_id(engine), _stream(x))
+    _lib.check(st, "scatter2scatter")
+    _credit(order, d_in, d_out)
+    if _fault_inject and out.numel():
+        out.view(-1)[0] += 0.01
+    return out
+
+
+def scatter_combine(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    order: GroupedOrder,
+    fan_out: int,
+    p_flat: torch.Tensor,
+    combine_cols: int,
+    grouped_in: bool,
+    tile: TileConfig | None = None,
+) -> torch.Tensor:
+    """scatter2scatter with the weighted slot-sum fused into the write (kernels.py:242-286).
+
+    The T*k pre-combine buffer never exists: the per-slot products are scaled by
+    p and accumulated into an fp32 (T, d_out) buffer, then rounded once.
+    """
+    if fan_out < 1:
+        raise ValueError(f"fan_out must be >= 1, got {fan_out}")
+    num_slots = order.num_slots
+    if num_slots % combine_cols:
+        raise ValueError(f"combine width {combine_cols} must divide T*k ({num_slots})")
+    require_dims(tuple(p_flat.shape) == (num_slots,), "combine weights", tuple(p_flat.shape), (num_slots,))
+    d_in, d_out = w.shape[1], w.shape[2]
+    require_dims(x.shape[1] == d_in, "input width vs expert weights", tuple(x.shape), (d_in, d_out))
+    if grouped_in:
+        require_dims(x.shape[0] == num_slots, "grouped input rows vs slots", (x.shape[0],), (num_slots,))
+    elif x.shape[0] * fan_out != num_slots:
+        raise ValueError(
+            f"scattered input rows ({x.shape[0]}) * fan_out ({fan_out}) must equal T*k ({num_slots})")
+    x, w = _cuda(x, "x"), _cuda(w, "w")
+    p32 = _cuda(p_flat.to(torch.float32), "p_flat")
+    rows = num_slots // combine_cols
+    acc = torch.empty((rows, d_out), dtype=torch.float32, device=x.device)
+    y = acc if x.dtype == torch.float32 else torch.empty((rows, d_out), dtype=x.dtype, device=x.device)
+    st = _lib.load().smoe_scatter_combine(
+        x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], d_in, d_out, order.o.data_ptr(),
+        order.bin_offsets.data_ptr(), num_slots, fan_out, p32.data_ptr(), combine_cols, int(grouped_in),
+        _dtype_id(x), acc.data_ptr(), y.data_ptr(), _stream(x))
+    _lib.check(st, "scatter_combine")
+    _credit(order, d_in, d_out)
+    return y
+
+
+def group(
+    x: torch.Tensor,
+    order: GroupedOrder,
+    weights: torch.Tensor | None = None,
+    fan_out: int = 1,
+    out: torch.Tensor | None = None,
+) -> torch.Tensor:
+    """Copy into grouped order: row i <- x[o[i] // fan_out] * weights[o[i]] (kernels.py:289-326)."""
+    if fan_out < 1:
+        raise ValueError(f"fan_out must be >= 1, got {fan_out}")
+    num_slots = order.num_slots
+    if x.shape[0] * fan_out != num_slots:
+        raise ValueError(f"input rows ({x.shape[0]}) * fan_out ({fan_out}) must equal T*k ({num_slots})")
+    if weights is not None:
+        require_dims(tuple(weights.shape) == (num_slots,), "slot weights", tuple(weights.shape), (num_slots,))
+        weights = _cuda(weights.to(torch.float32), "weights")
+    x = _cuda(x, "x")
+    if out is None:
+        out = torch.empty((num_slots, x.shape[1]), dtype=x.dtype, device=x.device)
+    else:
+        require_dims(tuple(out.shape) == (num_slots, x.shape[1]), "out buffer", tuple(out.shape),
+                     (num_slots, x.shape[1]))
+        if out.dtype != x.dtype:
+            raise ValueError(f"out dtype {out.dtype} does not match input dtype {x.dtype}")
+    st = _lib.load().smoe_group(x.data_ptr(), x.shape[0], x.shape[1], order.o.data_ptr(), num_slots,
+                                fan_out, _ptr(weights), _dtype_id(x), out.data_ptr(), _stream(x))
+    _lib.check(st, "group")
+    return out
+
+
+def group_xty(
+    xg: torch.Tensor,
+    yg: torch.Tensor,
+    order: GroupedOrder,
+    tile: TileConfig | None = None,
+    *,
+    out: torch.Tensor | None = None,
+    engine: str | None = None,
+) -> torch.Tensor:
+    """Per-expert Gram blocks dW[e] = Xg[bin e]^T @ Yg[bin e]; empty bin -> 0 (kernels.py:329-361)."""
+    num_slots = order.num_slots
+    require_dims(xg.shape[0] == num_slots, "grouped X rows vs slots", (xg.shape[0],), (num_slots,))
+    require_dims(yg.shape[0] == num_slots, "grouped Y rows vs slots", (yg.shape[0],), (num_slots,))
+    if xg.dtype != yg.dtype:
+        raise ValueError(f"group_xty operands must share a dtype, got {xg.dtype} and {yg.dtype}")
+    xg, yg = _cuda(xg, "xg"), _cuda(yg, "yg")
+    d_in, d_out = xg.shape[1], yg.shape[1]
+    e = order.num_experts
+    if out is None:
+        out = torch.empty((e, d_in, d_out), dtype=xg.dtype, device=xg.device)
+    else:
+        require_dims(tuple(out.shape) == (e, d_in, d_out), "dw buffer", tuple(out.shape), (e, d_in, d_out))
+    st = _lib.load().smoe_group_xty(xg.data_ptr(), yg.data_ptr(), order.bin_offsets.data_ptr(), e,
+                                    num_slots, d_in, d_out, _dtype_id(xg), out.data_ptr(),
+                                    _engine_id(engine), _stream(xg))
+    _lib.check(st, "group_xty")
+    _credit(order, d_in, d_out)
+    return out
+
+
+# ---- row kernels used by parallel_linear (not in the reference's kernels.py) ----
+
+def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Y[s] = sum_i p[s, i] * Y_hat[s*j + i]  (parallel_linear.py:69-73)."""
+    s, j = p.shape
+    y_hat = _cuda(y_hat, "y_hat")
+    p32 = _cuda(p.to(torch.float32), "p")
+    if out is None:
+        out = torch.empty((s, y_hat.shape[1]), dtype=y_hat.dtype, device=y_hat.device)
+    st = _lib.load().smoe_combine(y_hat.data_ptr(), p32.data_ptr(), s, j, y_hat.shape[1],
+                                  _dtype_id(y_hat), out.data_ptr(), _stream(y_hat))
+    _lib.check(st, "combine")
+    return out
+
+
+def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int) -> torch.Tensor:
+    """dp[s, i] = <dY[s], Y_hat[s*j + i]>  (parallel_linear.py:198-206), float32."""
+    dy, y_hat = _cuda(dy, "dy"), _cuda(y_hat, "y_hat")
+    dp = torch.empty((s, j), dtype=torch.float32, device=dy.device)
+    st = _lib.load().smoe_combine_grad_p(dy.data_ptr(), y_hat.data_ptr(), s, j, dy.shape[1],
+                                         _dtype_id(dy), dp.data_ptr(), _stream(dy))
+    _lib.check(st, "combine_grad_p")
+    return dp
+
+
+def fanout_reduce(slot_grads: torch.Tensor, fan_out: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """dX[t] = sum_j G[t*fan_out + j]  (parallel_linear.py:259-266)."""
+    g = _cuda(slot_grads, "slot_grads")
+    t = g.shape[0] // fan_out
+    if out is None:
+        out = torch.empty((t, g.shape[1]), dtype=g.dtype, device=g.device)
+    st = _lib.load().smoe_fanout_reduce(g.data_ptr(), t, fan_out, g.shape[1], _dtype_id(g),
+                                        out.data_ptr(), _stream(g))
+    _lib.check(st, "fanout_reduce")
+    return out
+
+
+def activation_kernel(x: torch.Tensor, name: str, derivative: bool,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """act(x) or act'(x), fp32 math, rounded once (moe_layers.py:75-83)."""
+    if name not in _lib.ACTIVATION_IDS:
+        raise ValueError(f"unknown activation {name!r}; choose from {sorted(_lib.ACTIVATION_IDS)}")
+    x = _cuda(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    st = _lib.load().smoe_apply_activation(x.data_ptr(), x.numel(), _lib.ACTIVATION_IDS[name],
+                                           int(derivative), _dtype_id(x), out.data_ptr(), _stream(x))
+    _lib.check(st, "activation")
+    return out

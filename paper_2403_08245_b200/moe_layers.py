@@ -1,0 +1,397 @@
+"""Routed layers built from the expert-linear transform (GPU).
+
+Mirrors the reference moe_layers.py (/root/reference/pkg/src/scattermlp/moe_layers.py):
+activations (:42-90), SmoeMlpConfig / init_smoe_mlp_weights (:93-121),
+smoe_mlp_forward / smoe_mlp_backward (:140-211), MomhaConfig / MomhaWeights /
+init_momha_weights (:214-267), attention / attention_backward (:280-377),
+momha_forward / momha_backward (:406-482).
+
+B200 changes (same results, fewer passes over HBM):
+  * the activation is fused into the first transform's epilogue, which writes
+    the retained pre-activation and the activated hidden state in one pass
+    (reference: copy + in-place activation, :169-175);
+  * the activation derivative is fused into the output transform's
+    input-gradient kernel (reference: a separate multiply, :205-206).
+The buffer-reuse discipline of smoe_mlp_backward (:198-211) is kept exactly.
+
+The attention core of MoMHA (between the two routed projections) is outside
+the ParallelLinear hot path; it runs as plain torch GPU ops.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from . import parallel_linear as pl
+from .errors import require_dims
+from .kernels import (
+    GROUPED_TO_SCATTERED,
+    SCATTERED_TO_GROUPED,
+    SCATTERED_TO_SCATTERED,
+    LayoutFlag,
+    TileConfig,
+)
+from .router import GroupedOrder, RoutingResult
+
+ACTIVATIONS = ("gelu", "relu", "silu")
+
+
+def _activation(name: str) -> str:
+    if name not in ACTIVATIONS:
+        raise ValueError(f"unknown activation {name!r}; choose from {sorted(ACTIVATIONS)}")
+    return name
+
+
+def apply_activation(values: torch.Tensor, name: str) -> torch.Tensor:
+    """Elementwise activation (fp32 math, rounded once), moe_layers.py:75-78."""
+    return K.activation_kernel(values, _activation(name), derivative=False)
+
+
+def activation_grad(pre: torch.Tensor, name: str) -> torch.Tensor:
+    """Elementwise activation derivative, moe_layers.py:81-83."""
+    return K.activation_kernel(pre, _activation(name), derivative=True)
+
+
+@dataclass(frozen=True)
+class SmoeMlpConfig:
+    """Shapes for the routed MLP: two expert stacks around one activation (moe_layers.py:93-108)."""
+
+    d_model: int
+    d_expert: int
+    num_experts: int
+    k: int
+    activation: str = "gelu"
+
+    def __post_init__(self):
+        if min(self.d_model, self.d_expert, self.num_experts, self.k) < 1:
+            raise ValueError(f"all MLP dimensions must be >= 1: {self}")
+        if self.k > self.num_experts:
+            raise ValueError(f"k={self.k} exceeds expert count {self.num_experts}")
+        _activation(self.activation)
+
+
+def seeded_expert_tensor(num_experts, d_in, d_out, seed, scale=1.0, dtype=torch.float32,
+                         device="cuda") -> torch.Tensor:
+    """U[-scale, scale] from PCG64(seed), the reference's draw (core_tensor.py:155-168)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    arr = rng.uniform(-scale, scale, size=(num_experts, d_in, d_out)).astype(np.float32)
+    return torch.from_numpy(arr).to(device=device, dtype=dtype)
+
+
+def seeded_matrix(rows, cols, seed, scale=1.0, dtype=torch.float32, device="cuda") -> torch.Tensor:
+    """U[-scale, scale] from PCG64(seed) (core_tensor.py:146-152)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    arr = rng.uniform(-scale, scale, size=(rows, cols)).astype(np.float32)
+    return torch.from_numpy(arr).to(device=device, dtype=dtype)
+
+
+def init_smoe_mlp_weights(config: SmoeMlpConfig, seed: int, dtype=torch.float32, device="cuda",
+                          source: str = "pcg64"):
+    """Seeded (W1, W2) expert stacks with 1/sqrt(d_in) scaling (moe_layers.py:111-121).
+
+    source="pcg64" reproduces the reference's bytes exactly (CPU draw, upload);
+    source="device" draws U[-s, s] with torch on the GPU (perf-only runs).
+    """
+    e, d, de = config.num_experts, config.d_model, config.d_expert
+    s1, s2 = 1.0 / math.sqrt(d), 1.0 / math.sqrt(de)
+    if source == "pcg64":
+        return (seeded_expert_tensor(e, d, de, seed, s1, dtype, device),
+                seeded_expert_tensor(e, de, d, seed + 1, s2, dtype, device))
+    g = torch.Generator(device=device).manual_seed(seed)
+    w1 = (torch.rand((e, d, de), generator=g, device=device, dtype=torch.float32) * 2 - 1).mul_(s1).to(dtype)
+    w2 = (torch.rand((e, de, d), generator=g, device=device, dtype=torch.float32) * 2 - 1).mul_(s2).to(dtype)
+    return w1, w2
+
+
+@dataclass
+class SmoeMlpContext:
+    hidden_ctx: pl.LinearContext
+    output_ctx: pl.LinearContext
+    h_pre: torch.Tensor
+    activation: str
+
+
+@dataclass
+class SmoeMlpGradients:
+    dx: torch.Tensor
+    dw1: torch.Tensor
+    dw2: torch.Tensor
+    dp: torch.Tensor
+
+
+def smoe_mlp_forward(
+    x: torch.Tensor,
+    w1: torch.Tensor,
+    w2: torch.Tensor,
+    routing: RoutingResult,
+    order: GroupedOrder,
+    *,
+    activation: str = "gelu",
+    training: bool = True,
+    tile: TileConfig | None = None,
+    ledger=None,
+) -> tuple[torch.Tensor, SmoeMlpContext | None]:
+    """Y[t] = sum_i p[t,i] * act(x[t] @ W1[e_i]) @ W2[e_i]  (moe_layers.py:140-182).
+
+    The hidden state exists only in grouped layout (T*k x d_expert).
+    """
+    require_dims(w1.shape[2] == w2.shape[1], "expert hidden widths", tuple(w1.shape[1:]), tuple(w2.shape[1:]))
+    require_dims(w1.shape[1] == x.shape[1], "input width vs W1", tuple(x.shape), tuple(w1.shape[1:]))
+    require_dims(w2.shape[2] == x.shape[1], "W2 output width vs model width", tuple(w2.shape[1:]), (x.shape[1],))
+    _activation(activation)
+    k = routing.k
+    if order.num_slots != x.shape[0] * k:
+        raise ValueError(f"order covers {order.num_slots} slots but routing implies {x.shape[0]}*{k}")
+    n, de = order.num_slots, w1.shape[2]
+    if training:
+        h_pre = torch.empty((n, de), dtype=x.dtype, device=x.device)
+        h = torch.empty((n, de), dtype=x.dtype, device=x.device)
+        K.scatter2scatter(x, w1, order, k, SCATTERED_TO_GROUPED, tile, out=h_pre,
+                          activation=activation, act_out=h)
+        if ledger:
+            ledger.alloc("mlp.hidden.y", n, de, "forward")
+            ledger.alloc("mlp.h_preactivation", n, de, "backward")
+        hidden_ctx = pl.LinearContext(x=x, w=w1, order=order, p=None, fan_out=k, x_was_grouped=False,
+                                      y_was_grouped=True, y_hat=h)
+    else:
+        h = K.scatter2scatter(x, w1, order, k, SCATTERED_TO_GROUPED, tile, activation=activation)
+        if ledger:
+            ledger.alloc("mlp.hidden.y", n, de, "forward")
+        h_pre = hidden_ctx = None
+    y, output_ctx = pl.forward(h, w2, order, p=routing.p, fan_out=1, layout=GROUPED_TO_SCATTERED,
+                               tile=tile, training=training, ledger=ledger, name="mlp.output")
+    if not training:
+        return y, None
+    return y, SmoeMlpContext(hidden_ctx=hidden_ctx, output_ctx=output_ctx, h_pre=h_pre, activation=activation)
+
+
+def smoe_mlp_backward(ctx: SmoeMlpContext, dy: torch.Tensor, *, tile: TileConfig | None = None,
+                      ledger=None) -> SmoeMlpGradients:
+    """Gradients for the routed MLP; stops at dp (moe_layers.py:185-211).
+
+    Reuse: the output transform's input gradients land in the activated hidden
+    buffer (after dW2 consumed it) with act'(h_pre) fused in; the retained
+    pre-combine output's storage takes the hidden transform's grouped input.
+    No new T*k-row buffer is allocated.
+    """
+    out_ctx = ctx.output_ctx
+    hid_ctx = ctx.hidden_ctx
+    out_ctx.scratch_grouped_x = out_ctx.x
+    g2 = pl.backward(out_ctx, dy, tile=tile, ledger=ledger, name="mlp.output",
+                     dx_activation_grad=(ctx.h_pre, ctx.activation))
+    dh = g2.dx
+    hid_ctx.scratch_grouped_x = out_ctx.y_hat
+    g1 = pl.backward(hid_ctx, dh, tile=tile, ledger=ledger, name="mlp.hidden")
+    return SmoeMlpGradients(dx=g1.dx, dw1=g1.dw, dw2=g2.dw, dp=g2.dp)
+
+
+class _SmoeMlpFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(actx, x, w1, w2, p, routing, order, activation):
+        y, mctx = smoe_mlp_forward(x.detach(), w1.detach(), w2.detach(), routing, order,
+                                   activation=activation, training=True)
+        actx.mctx = mctx
+        return y
+
+    @staticmethod
+    def backward(actx, dy):
+        g = smoe_mlp_backward(actx.mctx, dy.contiguous())
+        actx.mctx = None
+        return g.dx, g.dw1, g.dw2, g.dp, None, None, None
+
+
+class SmoeMlp(torch.nn.Module):
+    """The SMoE MLP module (north_star): two expert stacks around one activation.
+
+    forward(x, routing, order) -> (T, d_model); differentiable wrt x, W1, W2 and p
+    (routing.p), through the fused GPU forward/backward above.
+    """
+
+    def __init__(self, config: SmoeMlpConfig, dtype=torch.bfloat16, device="cuda", seed: int = 0,
+                 source: str = "device"):
+        super().__init__()
+        self.config = config
+        w1, w2 = init_smoe_mlp_weights(config, seed, dtype=dtype, device=device, source=source)
+        self.w1 = torch.nn.Parameter(w1)
+        self.w2 = torch.nn.Parameter(w2)
+
+    def forward(self, x: torch.Tensor, routing: RoutingResult, order: GroupedOrder) -> torch.Tensor:
+        if not self.training and not torch.is_grad_enabled():
+            y, _ = smoe_mlp_forward(x, self.w1, self.w2, routing, order, activation=self.config.activation,
+                                    training=False)
+            return y
+        return _SmoeMlpFunction.apply(x, self.w1, self.w2, routing.p, routing, order, self.config.activation)
+
+
+# ---------------------------------------------------------------------------
+# Mixture of multi-head attention (MoMHA): routed query / output projections.
+
+@dataclass(frozen=True)
+class MomhaConfig:
+    """Routed multi-head attention shapes (moe_layers.py:214-247)."""
+
+    d_model: int
+    d_head: int
+    num_heads: int
+    heads_per_expert: int
+    num_experts: int
+    k: int
+    causal: bool = True
+
+    def __post_init__(self):
+        if min(self.d_model, self.d_head, self.num_heads, self.heads_per_expert, self.num_experts, self.k) < 1:
+            raise ValueError(f"all attention dimensions must be >= 1: {self}")
+        if self.num_heads != self.k * self.heads_per_expert:
+            raise ValueError(f"num_heads ({self.num_heads}) must equal k ({self.k}) * "
+                             f"heads_per_expert ({self.heads_per_expert})")
+        if self.k > self.num_experts:
+            raise ValueError(f"k={self.k} exceeds expert count {self.num_experts}")
+
+    @property
+    def d_proj(self) -> int:
+        return self.heads_per_expert * self.d_head
+
+
+@dataclass
+class MomhaWeights:
+    wq: torch.Tensor  # (E, d_model, d_proj)
+    wk: torch.Tensor  # (d_model, d_proj), shared
+    wv: torch.Tensor  # (d_model, d_proj), shared
+    wo: torch.Tensor  # (E, d_proj, d_model)
+
+
+def init_momha_weights(config: MomhaConfig, seed: int, dtype=torch.float32, device="cuda") -> MomhaWeights:
+    """Seeded MoMHA weights, same draws as moe_layers.py:257-267."""
+    d, dp_ = config.d_model, config.d_proj
+    s_in, s_out = 1.0 / math.sqrt(d), 1.0 / math.sqrt(dp_)
+    return MomhaWeights(
+        wq=seeded_expert_tensor(config.num_experts, d, dp_, seed, s_in, dtype, device),
+        wk=seeded_matrix(d, dp_, seed + 1, s_in, dtype, device),
+        wv=seeded_matrix(d, dp_, seed + 2, s_in, dtype, device),
+        wo=seeded_expert_tensor(config.num_experts, dp_, d, seed + 3, s_out, dtype, device),
+    )
+
+
+def _attn_core(q, keys, values, seq_len, d_head, k, causal):
+    """Slot queries (T*k, d_proj) in chronological order vs dense K/V (T, d_proj).
+
+    Query head (slot, j) attends with K/V head j of its sequence; causal within
+    the sequence (moe_layers.py:280-327).  float32 math.
+    """
+    n = keys.shape[0]
+    b = n // seq_len
+    h = q.shape[1] // d_head
+    qf = q.float().view(b, seq_len * k, h, d_head).transpose(1, 2)          # (b, h, L*k, dh)
+    kf = keys.float().view(b, seq_len, h, d_head).transpose(1, 2)           # (b, h, L, dh)
+    vf = values.float().view(b, seq_len, h, d_head).transpose(1, 2)
+    scores = (qf @ kf.transpose(-1, -2)) * (1.0 / math.sqrt(d_head))        # (b, h, L*k, L)
+    if causal:
+        qt = torch.arange(seq_len * k, device=q.device) // k
+        kt = torch.arange(seq_len, device=q.device)
+        scores = scores.masked_fill(qt[:, None] < kt[None, :], float("-inf"))
+    probs = torch.softmax(scores, dim=-1)
+    out = probs @ vf                                                         # (b, h, L*k, dh)
+    return out.transpose(1, 2).reshape(b * seq_len * k, h * d_head)
+
+
+def attention(q, keys, values, slot_tokens, seq_len, d_head, causal=True):
+    """Scaled dot-product attention over per-slot queries (moe_layers.py:280-327).
+
+    Slots must be chronological (slot s belongs to token s // k), as momha_forward produces.
+    """
+    require_dims(q.shape[1] == keys.shape[1] == values.shape[1], "projection widths", (q.shape[1],),
+                 (keys.shape[1], values.shape[1]))
+    if q.shape[1] % d_head:
+        raise ValueError(f"projection width {q.shape[1]} is not divisible by d_head {d_head}")
+    n = keys.shape[0]
+    if n % seq_len:
+        raise ValueError(f"token count {n} is not divisible by seq_len {seq_len}")
+    k = q.shape[0] // n
+    return _attn_core(q, keys, values, seq_len, d_head, k, causal).to(q.dtype)
+
+
+def attention_backward(q, keys, values, slot_tokens, seq_len, d_head, causal, d_out):
+    """(dq, dkeys, dvalues) by recomputation (moe_layers.py:330-377)."""
+    n = keys.shape[0]
+    k = q.shape[0] // n
+    with torch.enable_grad():
+        qv = q.detach().float().requires_grad_(True)
+        kv = keys.detach().float().requires_grad_(True)
+        vv = values.detach().float().requires_grad_(True)
+        out = _attn_core(qv, kv, vv, seq_len, d_head, k, causal)
+        dq, dk, dv = torch.autograd.grad(out, (qv, kv, vv), d_out.float())
+    return dq.to(q.dtype), dk.to(q.dtype), dv.to(q.dtype)
+
+
+@dataclass
+class MomhaContext:
+    query_ctx: pl.LinearContext
+    output_ctx: pl.LinearContext
+    x: torch.Tensor
+    q: torch.Tensor
+    keys: torch.Tensor
+    values: torch.Tensor
+    wk: torch.Tensor
+    wv: torch.Tensor
+    slot_tokens: torch.Tensor | None
+    seq_len: int
+    d_head: int
+    causal: bool
+
+
+@dataclass
+class MomhaGradients:
+    dx: torch.Tensor
+    dwq: torch.Tensor
+    dwk: torch.Tensor
+    dwv: torch.Tensor
+    dwo: torch.Tensor
+    dp: torch.Tensor
+
+
+def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: GroupedOrder,
+                  config: MomhaConfig, seq_len: int, *, training: bool = True,
+                  tile: TileConfig | None = None, ledger=None):
+    """Routed attention over flattened tokens (moe_layers.py:406-457).
+
+    The two routed projections are ParallelLinear calls with chronological
+    (scattered->scattered) layout, exactly the reference's :438-449.
+    """
+    n = x.shape[0]
+    require_dims(x.shape[1] == config.d_model, "input width", tuple(x.shape), (config.d_model,))
+    if n % seq_len:
+        raise ValueError(f"token count {n} is not divisible by seq_len {seq_len}")
+    if routing.num_tokens != n or routing.k != config.k:
+        raise ValueError(f"routing covers {routing.num_tokens} tokens with k={routing.k}; "
+                         f"expected {n} tokens with k={config.k}")
+    keys = (x.float() @ weights.wk.float()).to(x.dtype)
+    values = (x.float() @ weights.wv.float()).to(x.dtype)
+    q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=SCATTERED_TO_SCATTERED,
+                              tile=tile, training=training, ledger=ledger, name="momha.query")
+    attn_out = attention(q, keys, values, None, seq_len, config.d_head, config.causal)
+    y, output_ctx = pl.forward(attn_out, weights.wo, order, p=routing.p, fan_out=1,
+                               layout=SCATTERED_TO_SCATTERED, tile=tile, training=training, ledger=ledger,
+                               name="momha.output")
+    if not training:
+        return y, None
+    return y, MomhaContext(query_ctx=query_ctx, output_ctx=output_ctx, x=x, q=q, keys=keys, values=values,
+                           wk=weights.wk, wv=weights.wv, slot_tokens=None, seq_len=seq_len,
+                           d_head=config.d_head, causal=config.causal)
+
+
+def momha_backward(ctx: MomhaContext, dy, *, tile: TileConfig | None = None, ledger=None) -> MomhaGradients:
+    """Gradients for routed attention; stops at dp (moe_layers.py:460-482)."""
+    g_o = pl.backward(ctx.output_ctx, dy, tile=tile, ledger=ledger, name="momha.output")
+    dq, dk, dv = attention_backward(ctx.q, ctx.keys, ctx.values, None, ctx.seq_len, ctx.d_head, ctx.causal,
+                                    g_o.dx)
+    g_q = pl.backward(ctx.query_ctx, dq, tile=tile, ledger=ledger, name="momha.query")
+    x32 = ctx.x.float()
+    dwk = (x32.t() @ dk.float()).to(ctx.x.dtype)
+    dwv = (x32.t() @ dv.float()).to(ctx.x.dtype)
+    dx_kv = dk.float() @ ctx.wk.float().t() + dv.float() @ ctx.wv.float().t()
+    dx = (g_q.dx.float() + dx_kv).to(ctx.x.dtype)
+    return MomhaGradients(dx=dx, dwq=g_q.dw, dwk=dwk, dwv=dwv, dwo=g_o.dw, dp=g_o.dp)

@@ -1,0 +1,172 @@
+"""scatter2scatter / group / group_xty / scatter_combine parity on the GPU.
+
+fp32 check mode (engine=simt): the reference's elementwise tolerance
+(rtol 1e-5, test_kernels.py:65) plus an absolute floor for fp32-vs-f64
+accumulation, and <= 1e-4 relative Frobenius (north_star).
+bf16 (engine auto -> tcgen05 when built): oracle fed the bf16-rounded inputs,
+relative Frobenius error <= 2e-2 per tensor (north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_08245_b200 as sm
+from conftest import load_golden
+from gpu_util import bf16_round, np_of, order_of, rel_err, t
+from oracle import scattermlp_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = {"s2g": sm.SCATTERED_TO_GROUPED, "g2s": sm.GROUPED_TO_SCATTERED,
+           "s2s": sm.SCATTERED_TO_SCATTERED, "g2g": sm.GROUPED_TO_GROUPED}
+FP32_RTOL, FP32_ATOL = 1e-5, 1e-6
+ENGINES = ["simt", "auto"]
+
+
+def test_golden_scatter2scatter_fp32():
+    g = load_golden("kernels")
+    for j in range(int(g["num_s2s"])):
+        pre = f"s2s{j}_"
+        order = order_of(g[pre + "idx"], int(g[pre + "E"]))
+        y = sm.scatter2scatter(t(g[pre + "x"]), t(g[pre + "w"]), order, int(g[pre + "fan_out"]),
+                               LAYOUTS[str(g[pre + "layout"])], transpose_w=bool(g[pre + "transpose"]))
+        np.testing.assert_allclose(np_of(y), g[pre + "y"], rtol=FP32_RTOL, atol=FP32_ATOL, err_msg=str(j))
+        assert rel_err(y, g[pre + "y"]) <= 1e-4
+
+
+def test_golden_group_xty_combine_fp32():
+    g = load_golden("kernels")
+    order = order_of(g["grp_idx"], 5)
+    np.testing.assert_array_equal(np_of(sm.group(t(g["grp_x"]), order, fan_out=2)), g["grp_plain"])
+    got = sm.group(t(g["grp_x"]), order, weights=t(g["grp_p"].reshape(-1)), fan_out=2)
+    np.testing.assert_allclose(np_of(got), g["grp_weighted"], rtol=1e-6, atol=1e-7)
+    order2 = order_of(g["xty_idx"], 6)
+    dw = sm.group_xty(t(g["xty_x"]), t(g["xty_y"]), order2)
+    np.testing.assert_allclose(np_of(dw), g["xty_dw"], rtol=FP32_RTOL, atol=FP32_ATOL)
+    assert float(dw[5].abs().max()) == 0.0  # skip_one: expert 5 has an empty bin
+    sc = sm.scatter_combine(t(g["grp_x"]), t(g["sc_w"]), order, 2, t(g["grp_p"].reshape(-1)), 2, False)
+    np.testing.assert_allclose(np_of(sc), g["sc_y"], rtol=FP32_RTOL, atol=FP32_ATOL)
+
+
+def _problem(rng, tokens, k, e, d_in, d_out, layout, transpose, flavor="gate"):
+    if flavor == "all_to_one":
+        idx = np.tile(np.arange(k), (tokens, 1))
+    elif flavor == "skip_one":
+        idx = np.stack([rng.permutation(e - 1)[:k] for _ in range(tokens)])
+    else:
+        idx = np.stack([rng.permutation(e)[:k] for _ in range(tokens)])
+    rows = tokens * k if layout.grouped_in else tokens
+    fan_out = 1 if layout.grouped_in else k
+    x = rng.uniform(-1, 1, (rows, d_in)).astype(np.float32)
+    shape = (e, d_out, d_in) if transpose else (e, d_in, d_out)
+    w = (rng.uniform(-1, 1, shape) / np.sqrt(d_in)).astype(np.float32)
+    return idx, x, w, fan_out
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("lname", list(LAYOUTS))
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("flavor", ["gate", "all_to_one", "skip_one"])
+def test_bf16_layouts_vs_oracle(engine, lname, transpose, flavor):
+    """Tile-sized and ragged shapes, bf16 storage, fp32 accumulate."""
+    rng = np.random.default_rng(hash((lname, transpose, flavor)) % 2**32)
+    layout = LAYOUTS[lname]
+    for tokens, k, e, d_in, d_out in [(300, 2, 6, 256, 512), (1000, 2, 8, 128, 256), (77, 3, 5, 64, 192)]:
+        idx, x, w, fan_out = _problem(rng, tokens, k, e, d_in, d_out, layout, transpose, flavor)
+        xb, wb = bf16_round(x), bf16_round(w)
+        o, off = orc.compute_grouped_order(idx, e)
+        want = orc.scatter2scatter(xb, wb, o, off, fan_out, layout.grouped_in, layout.grouped_out, transpose)
+        order = order_of(idx, e)
+        y = sm.scatter2scatter(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out, layout,
+                               transpose_w=transpose, engine=engine)
+        assert y.dtype == torch.bfloat16
+        assert rel_err(y, want) <= 2e-2, (tokens, k, e, d_in, d_out)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_layout_consistency_bit_identical(engine):
+    """grouped-out composed with the inverse permutation == scattered-out (test_acceptance.py:349-381)."""
+    rng = np.random.default_rng(6)
+    for dtype in (torch.float32, torch.bfloat16):
+        idx, x, w, fan_out = _problem(rng, 500, 2, 8, 128, 256, sm.SCATTERED_TO_GROUPED, False)
+        order = order_of(idx, 8)
+        xt, wt = t(x, dtype), t(w, dtype)
+        grouped = sm.scatter2scatter(xt, wt, order, fan_out, sm.SCATTERED_TO_GROUPED, engine=engine)
+        scattered = sm.scatter2scatter(xt, wt, order, fan_out, sm.SCATTERED_TO_SCATTERED, engine=engine)
+        assert torch.equal(grouped[order.inverse().long()], scattered)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_out_reuse_and_determinism_bit_identical(engine):
+    rng = np.random.default_rng(8)
+    idx, x, w, _ = _problem(rng, 400, 2, 8, 128, 128, sm.GROUPED_TO_SCATTERED, False)
+    order = order_of(idx, 8)
+    xt, wt = t(x, torch.bfloat16), t(w, torch.bfloat16)
+    fresh = sm.scatter2scatter(xt, wt, order, 1, sm.GROUPED_TO_SCATTERED, engine=engine)
+    out = torch.full_like(fresh, float("nan"))
+    reused = sm.scatter2scatter(xt, wt, order, 1, sm.GROUPED_TO_SCATTERED, out=out, engine=engine)
+    assert reused.data_ptr() == out.data_ptr()
+    assert torch.equal(fresh, reused)
+    again = sm.scatter2scatter(xt, wt, order, 1, sm.GROUPED_TO_SCATTERED, engine=engine)
+    assert torch.equal(fresh, again)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("flavor", ["gate", "all_to_one", "skip_one"])
+def test_group_xty_bf16(engine, flavor):
+    rng = np.random.default_rng(11)
+    e = 6
+    for n_tok, k, d_in, d_out in [(600, 2, 128, 256), (333, 2, 256, 128), (50, 1, 64, 64)]:
+        idx, _, _, _ = _problem(rng, n_tok, k, e, 8, 8, sm.SCATTERED_TO_GROUPED, False, flavor)
+        order = order_of(idx, e)
+        n = n_tok * k
+        xg = bf16_round(rng.uniform(-1, 1, (n, d_in)).astype(np.float32))
+        yg = bf16_round(rng.uniform(-1, 1, (n, d_out)).astype(np.float32))
+        o, off = orc.compute_grouped_order(idx, e)
+        want = orc.group_xty(xg, yg, off)
+        dw = sm.group_xty(t(xg, torch.bfloat16), t(yg, torch.bfloat16), order, engine=engine)
+        assert rel_err(dw, want) <= 2e-2
+        counts = np.diff(off)
+        for ee in np.nonzero(counts == 0)[0]:
+            assert float(dw[ee].float().abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("act", ["gelu", "relu", "silu"])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_fused_activation_epilogues(act, engine):
+    rng = np.random.default_rng(12)
+    idx, x, w, fan_out = _problem(rng, 300, 2, 8, 128, 256, sm.SCATTERED_TO_GROUPED, False)
+    xb, wb = bf16_round(x), bf16_round(w)
+    order = order_of(idx, 8)
+    o, off = orc.compute_grouped_order(idx, 8)
+    pre = torch.empty((600, 256), dtype=torch.bfloat16, device="cuda")
+    h = torch.empty_like(pre)
+    sm.scatter2scatter(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, 2, sm.SCATTERED_TO_GROUPED,
+                       out=pre, activation=act, act_out=h, engine=engine)
+    want_pre = orc.scatter2scatter(xb, wb, o, off, 2, False, True)
+    assert rel_err(pre, want_pre) <= 2e-2
+    want_h = orc.act(np_of(pre), act)            # act of the stored (rounded) pre-activation
+    assert rel_err(h, want_h) <= 1e-2
+    # act-grad epilogue on a G2G transposed product
+    dyg = bf16_round(rng.uniform(-1, 1, (600, 128)).astype(np.float32))
+    w2 = bf16_round((rng.uniform(-1, 1, (8, 256, 128)) / 16).astype(np.float32))
+    dh = torch.empty_like(pre)
+    sm.scatter2scatter(t(dyg, torch.bfloat16), t(w2, torch.bfloat16), order, 1, sm.GROUPED_TO_GROUPED,
+                       transpose_w=True, out=dh, activation=act, act_grad_of=pre, engine=engine)
+    want_dh = orc.scatter2scatter(dyg, w2, o, off, 1, True, True, transpose_w=True) * orc.act_grad(np_of(pre), act)
+    assert rel_err(dh, want_dh) <= 2e-2
+
+
+def test_row_kernels_bf16():
+    rng = np.random.default_rng(13)
+    tokens, k, d = 1000, 2, 512
+    p = rng.random((tokens, k)).astype(np.float32)
+    y_hat = bf16_round(rng.uniform(-1, 1, (tokens * k, d)).astype(np.float32))
+    dy = bf16_round(rng.uniform(-1, 1, (tokens, d)).astype(np.float32))
+    yh = t(y_hat, torch.bfloat16)
+    y = sm.kernels.combine(t(p), yh)
+    assert rel_err(y, orc.combine(p, y_hat)) <= 1e-2
+    dp = sm.kernels.combine_grad_p(t(dy, torch.bfloat16), yh, tokens, k)
+    assert rel_err(dp, orc.combine_grad_p(dy, y_hat, tokens, k)) <= 1e-4
+    dx = sm.kernels.fanout_reduce(yh, k)
+    assert rel_err(dx, orc.fanout_reduce(y_hat, k)) <= 1e-2

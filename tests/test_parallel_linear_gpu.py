@@ -1,0 +1,99 @@
+"""ParallelLinear forward/backward parity (parallel_linear.py:85-269) on the GPU."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_08245_b200 as sm
+from conftest import load_golden
+from gpu_util import np_of, order_of, rel_err, t
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = {"s2g": sm.SCATTERED_TO_GROUPED, "g2s": sm.GROUPED_TO_SCATTERED,
+           "s2s": sm.SCATTERED_TO_SCATTERED, "g2g": sm.GROUPED_TO_GROUPED}
+
+
+def _case(g, j):
+    pre = f"pl{j}_"
+    order = order_of(g[pre + "idx"], int(g[pre + "E"]))
+    p = t(g[pre + "p"]) if int(g[pre + "p_given"]) else None
+    return pre, order, p, LAYOUTS[str(g[pre + "layout"])], int(g[pre + "fan_out"])
+
+
+def test_golden_forward_backward_fp32():
+    g = load_golden("parallel_linear")
+    for j in range(int(g["num_pl"])):
+        pre, order, p, layout, fan = _case(g, j)
+        y, ctx = sm.parallel_linear_forward(t(g[pre + "x"]), t(g[pre + "w"]), order, p=p, fan_out=fan,
+                                            layout=layout)
+        np.testing.assert_allclose(np_of(y), g[pre + "y"], rtol=1e-5, atol=1e-6)
+        gr = sm.parallel_linear_backward(ctx, t(g[pre + "dy"]))
+        np.testing.assert_allclose(np_of(gr.dx), g[pre + "dx"], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(np_of(gr.dw), g[pre + "dw"], rtol=1e-5, atol=1e-5)
+        if p is not None:
+            np.testing.assert_allclose(np_of(gr.dp), g[pre + "dp"], rtol=1e-5, atol=1e-5)
+        for got, name in ((gr.dx, "dx"), (gr.dw, "dw")):
+            assert rel_err(got, g[pre + name]) <= 1e-4
+
+
+def test_context_single_use_and_aliasing_rules():
+    g = load_golden("parallel_linear")
+    pre, order, p, layout, fan = _case(g, 4)   # a p-given case
+    assert p is not None
+    x, w = t(g[pre + "x"]), t(g[pre + "w"])
+    y, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    dy = t(g[pre + "dy"])
+    sm.parallel_linear_backward(ctx, dy)
+    with pytest.raises(RuntimeError, match="consumed"):
+        sm.parallel_linear_backward(ctx, dy)
+    y, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    with pytest.raises(RuntimeError, match="alias"):
+        sm.parallel_linear_backward(ctx, ctx.y_hat[: dy.shape[0]])
+    # scratch slots must not alias each other
+    y, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    n = order.num_slots
+    buf = torch.empty((n, max(x.shape[1], w.shape[2])), device="cuda")
+    ctx.scratch_grouped_dy = buf[:, : w.shape[2]]
+    ctx.scratch_grouped_x = buf[:, : x.shape[1]]
+    with pytest.raises(RuntimeError, match="alias"):
+        sm.parallel_linear_backward(ctx, dy)
+
+
+def test_seeded_scratch_is_bit_identical():
+    """test_parallel_linear.py:175-200: seeded scratch gives identical results."""
+    g = load_golden("parallel_linear")
+    pre, order, p, layout, fan = _case(g, 4)
+    x, w, dy = t(g[pre + "x"]), t(g[pre + "w"]), t(g[pre + "dy"])
+    _, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    base = sm.parallel_linear_backward(ctx, dy)
+    _, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    n = order.num_slots
+    ctx.scratch_grouped_dy = torch.empty((n, w.shape[2]), device="cuda")
+    ctx.scratch_grouped_x = torch.empty((n, w.shape[1]), device="cuda")
+    other = sm.parallel_linear_backward(ctx, dy)
+    assert torch.equal(base.dx, other.dx) and torch.equal(base.dw, other.dw) and torch.equal(base.dp, other.dp)
+
+
+def test_autograd_function_matches_functional():
+    g = load_golden("parallel_linear")
+    pre, order, p, layout, fan = _case(g, 4)
+    x = t(g[pre + "x"]).requires_grad_(True)
+    w = t(g[pre + "w"]).requires_grad_(True)
+    pp = p.clone().requires_grad_(True)
+    y = sm.ParallelLinear.apply(x, w, order, fan, pp, layout.grouped_in, False)
+    y.backward(t(g[pre + "dy"]))
+    np.testing.assert_allclose(np_of(y), g[pre + "y"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(np_of(x.grad), g[pre + "dx"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(np_of(w.grad), g[pre + "dw"], rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(np_of(pp.grad), g[pre + "dp"], rtol=1e-5, atol=1e-5)
+
+
+def test_inference_combine_equals_training():
+    """train == infer (test_parallel_linear.py:50-57), fp32 check mode."""
+    g = load_golden("parallel_linear")
+    pre, order, p, layout, fan = _case(g, 4)
+    x, w = t(g[pre + "x"]), t(g[pre + "w"])
+    y_train, _ = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout)
+    y_inf, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout, training=False)
+    assert ctx is None
+    np.testing.assert_allclose(np_of(y_inf), np_of(y_train), rtol=1e-5, atol=1e-6)
