@@ -36,6 +36,7 @@ int simt_scatter2scatter(const void *, const void *, int, int64_t, int64_t, cons
 int simt_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int, void *, cudaStream_t);
 int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, const float *, int, int, int, float *, void *, cudaStream_t);
 bool tc_available();
+bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out);
 int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int tc_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
 
@@ -95,7 +96,9 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
   REQUIRE(epilogue != SMOE_EPI_ACT_GRAD || aux, SMOE_EINVAL, "EPI_ACT_GRAD needs aux");
   if (n == 0) return SMOE_OK;
   REQUIRE(x && w && order && expert_offsets && out, SMOE_EINVAL, "scatter2scatter: null pointer");
-  bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available());
+  const int64_t d_in = transpose_w ? w_cols : w_rows, d_out = transpose_w ? w_rows : w_cols;
+  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
+                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && tc_supports_s2s(d_in, d_out, x, w, out));
   if (use_tc) {
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
     return tc_scatter2scatter(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
@@ -112,7 +115,9 @@ int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets
   REQUIRE(num_experts >= 1, SMOE_EINVAL, "num_experts must be >= 1");
   REQUIRE(dw && expert_offsets, SMOE_EINVAL, "group_xty: null pointer");
   REQUIRE(n == 0 || (xg && yg), SMOE_EINVAL, "group_xty: null pointer");
-  bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available());
+  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
+                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && n > 0 &&
+                 tc_supports_s2s(d_in, d_out, xg, yg, dw));
   if (use_tc) {
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only");
     return tc_group_xty(xg, yg, expert_offsets, num_experts, n, d_in, d_out, dw, S(stream));

@@ -1,0 +1,30 @@
+"""Run one GEMM variant a few times (target for ncu -k regex:tc_gemm)."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2403_08245_b200 as sm  # noqa: E402
+
+which = sys.argv[1]
+T, d, de, E, k = 32768, 4096, 14336, 8, 2
+n = T * k
+dev = "cuda"
+g = torch.Generator(device=dev).manual_seed(0)
+x = (torch.rand(T, d, device=dev, generator=g) * 2 - 1).bfloat16()
+xg = (torch.rand(n, d, device=dev, generator=g) * 2 - 1).bfloat16()
+w = ((torch.rand(E, d, de, device=dev, generator=g) * 2 - 1) / d ** 0.5).bfloat16()
+routing = sm.topk_select(torch.softmax(torch.randn(T, E, device=dev, generator=g), 1), k)
+order = sm.compute_grouped_order(routing)
+h = torch.empty(n, de, device=dev, dtype=torch.bfloat16)
+h2 = torch.empty_like(h)
+for _ in range(3):
+    if which == "l1":
+        sm.scatter2scatter(x, w, order, k, sm.SCATTERED_TO_GROUPED, out=h, activation="gelu", act_out=h2)
+    elif which == "dh":
+        sm.scatter2scatter(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, out=h2,
+                           activation="gelu", act_grad_of=h)
+    elif which == "l2":
+        sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
+torch.cuda.synchronize()
