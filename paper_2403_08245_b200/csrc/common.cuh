@@ -45,6 +45,47 @@ __device__ __forceinline__ float act_grad(int act, float z) {
   return s * (1.0f + z * (1.0f - s));
 }
 
+// Fast variants for the bf16 tensor-core epilogues.  erf uses Abramowitz &
+// Stegun 7.1.26 (|error| <= 1.5e-7, plus MUFU rcp/ex2 rounding, ~3e-7 total) —
+// three orders of magnitude below the bf16 rounding (2^-9) applied to the
+// result, so the exact-erf GELU semantics of the reference are kept.  The
+// fp32 check mode (SIMT kernels) uses act_fwd/act_grad above.
+struct ErfExp {
+  float erf;   // erf(z / sqrt(2))
+  float gexp;  // exp(-z^2 / 2)
+};
+__device__ __forceinline__ ErfExp erf_scaled(float z) {
+  const float x = fabsf(z) * 0.70710678118654752f;
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
+  float poly = fmaf(1.061405429f, t, -1.453152027f);
+  poly = fmaf(poly, t, 1.421413741f);
+  poly = fmaf(poly, t, -0.284496736f);
+  poly = fmaf(poly, t, 0.254829592f);
+  poly *= t;
+  const float e = __expf(-0.5f * z * z);
+  const float y = fmaf(-poly, e, 1.0f);
+  return {copysignf(y, z), e};
+}
+
+__device__ __forceinline__ float act_fwd_fast(int act, float z) {
+  if (act == SMOE_ACT_GELU) {
+    const ErfExp r = erf_scaled(z);
+    return 0.5f * z * (1.0f + r.erf);
+  }
+  if (act == SMOE_ACT_RELU) return z > 0.0f ? z : 0.0f;
+  return __fdividef(z, 1.0f + __expf(-z));
+}
+
+__device__ __forceinline__ float act_grad_fast(int act, float z) {
+  if (act == SMOE_ACT_GELU) {
+    const ErfExp r = erf_scaled(z);
+    return fmaf(z * 0.39894228040143268f, r.gexp, 0.5f * (1.0f + r.erf));
+  }
+  if (act == SMOE_ACT_RELU) return z > 0.0f ? 1.0f : 0.0f;
+  const float s = __fdividef(1.0f, 1.0f + __expf(-z));
+  return s * (1.0f + z * (1.0f - s));
+}
+
 inline int num_sms() {
   static int sms = -1;
   if (sms < 0) {

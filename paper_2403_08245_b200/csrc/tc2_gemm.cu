@@ -1,0 +1,448 @@
+// 2-CTA (cta_group::2) tcgen05 grouped GEMM: the default bf16 engine.
+//
+// Same GEMM family as tc_gemm.cu (scatter2scatter grouped-M, group_xty
+// grouped-K; see that file's header), but each tile is 256 x 256 and is
+// computed by a CTA pair on the two SMs of a TPC:
+//   * CTA rank r loads A rows [m0 + 128 r, +128) and B columns [n0 + 128 r, +128)
+//     into its own shared memory (32 KB per stage, 6 stages);
+//   * the leader (rank 0) issues tcgen05.mma.cta_group::2 (M=256, N=256, K=16),
+//     which reads both CTAs' operands and accumulates rows 128 r.. into each
+//     CTA's own TMEM (2 x 256 columns, double-buffered);
+//   * each CTA's epilogue drains its own TMEM rows.
+// Halving the B bytes each SM stages and reads per MMA is what lets the tensor
+// pipe run at full rate (SURVEY.md §7 "2-CTA 256-row tiles").
+//
+// Synchronisation (mbarriers; "L" = leader only):
+//   lfull[s]  per CTA: its own TMA bytes (+128 cp.async gather arrivals) landed
+//   pready[s] L: the peer's stage s is ready (peer relay warp arrives remotely
+//             after optional K-tail zeroing)
+//   empty[s]  per CTA: the leader's MMAs consumed stage s (multicast commit)
+//   tfull[a]  per CTA: accumulator a complete (multicast commit)
+//   tempty[a] L: both CTAs' epilogues drained accumulator a (16 arrivals)
+#include "tc_common.cuh"
+
+namespace smoe {
+namespace tc2 {
+
+using namespace smoe::tc;
+
+constexpr int TM = 256, TN = 256, BK = 64, STAGES = 6;
+constexpr int HM = TM / 2, HN = TN / 2;  // per-CTA halves
+constexpr int A_BYTES = HM * BK * 2;     // 16 KB
+constexpr int B_BYTES = HN * BK * 2;     // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;
+constexpr int EPI_WARPS = 8;
+constexpr int GATHER_WARPS = 4;
+constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
+__host__ __device__ constexpr int kernel_threads(int am) {
+  return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
+}
+
+template <int AM, int BMODE, bool GK>
+__global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 1)
+    tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, Params p) {
+  constexpr int THREADS = kernel_threads(AM);
+  // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
+  // critical producer and MMA warps take the highest ids and never queue behind
+  // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
+  constexpr int WP = EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0);
+  constexpr int WM = WP + 1;
+  constexpr bool RELAY = (AM == A_GATHER);  // cp.async data cannot signal the leader's barrier
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *tiles_smem = smem;
+  uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  uint64_t *lfull_bar = bars;                    // [STAGES]
+  uint64_t *pready_bar = bars + STAGES;          // [STAGES]
+  uint64_t *empty_bar = bars + 2 * STAGES;       // [STAGES]
+  uint64_t *tfull_bar = bars + 3 * STAGES;       // [2]
+  uint64_t *tempty_bar = bars + 3 * STAGES + 2;  // [2]
+  uint32_t *s_tmem = (uint32_t *)(bars + 3 * STAGES + 4);
+  int64_t *s_start = (int64_t *)(bars + 3 * STAGES + 6);  // [E+1]
+  int32_t *s_off = (int32_t *)(s_start + p.E + 1);         // [E+1]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t nN = (p.N + TN - 1) / TN;
+  const int64_t mM = (p.M + TM - 1) / TM;
+  const int64_t cluster_id = blockIdx.x >> 1;
+  const int64_t num_clusters = gridDim.x >> 1;
+
+  for (int i = threadIdx.x; i <= p.E; i += THREADS) s_off[i] = p.offsets[i];
+  if (warp == WP && lane == 0) {
+    prefetch_tmap(&tma_a);
+    prefetch_tmap(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&lfull_bar[s]), AM == A_GATHER ? 1 + 32 * GATHER_WARPS : 1);
+      mbar_init(smem_u32(&pready_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&tfull_bar[s]), 1);
+      mbar_init(smem_u32(&tempty_bar[s]), 2 * EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == WM) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int e = 0; e < p.E; ++e) {
+      s_start[e] = acc;
+      if (!GK) acc += ((s_off[e + 1] - s_off[e] + TM - 1) / TM) * nN;
+      else acc += mM * nN;
+    }
+    s_start[p.E] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  const int64_t total = s_start[p.E];
+
+  if (warp == WP) {
+    // ===================== TMA producer (own halves of A and B) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
+        const int n_half = (int)(tl.n0 + HN * rank);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          const uint32_t fb = smem_u32(&lfull_bar[stage]);
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+          const int kk = kb * BK;
+          if (RELAY) {
+            // gather mode: this CTA's bytes are counted locally and relayed
+            mbar_expect_tx(fb, B_BYTES);
+            if (BMODE == B_W_MN) {
+              tma_load_3d(&tma_b, fb, sb, n_half, kk, tl.e);
+              tma_load_3d(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
+            } else {
+              tma_load_3d(&tma_b, fb, sb, kk, n_half, tl.e);
+            }
+          } else {
+            // both CTAs' bytes are counted on the leader's barrier
+            if (leader) mbar_expect_tx(fb, 2 * STAGE_BYTES);
+            if (BMODE == B_W_MN) {
+              tma_load_3d_cg2(&tma_b, fb, sb, n_half, kk, tl.e);
+              tma_load_3d_cg2(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
+            } else if (BMODE == B_W_K) {
+              tma_load_3d_cg2(&tma_b, fb, sb, kk, n_half, tl.e);
+            } else {
+              tma_load_2d_cg2(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
+              tma_load_2d_cg2(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
+            }
+            if (AM == A_ROWS) {
+              tma_load_2d_cg2(&tma_a, fb, sa, kk, m_half);
+            } else if (AM == A_MN) {
+              tma_load_2d_cg2(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
+              tma_load_2d_cg2(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+            }
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      // Producer tail: wait until every stage's last fill was consumed, so no
+      // multicast commit can still be in flight to this CTA when it exits.
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == WM) {
+    if (leader) {
+      // ===================== MMA issuer (leader CTA) =====================
+      constexpr uint32_t a_mn = (AM == A_MN) ? 1u : 0u;
+      constexpr uint32_t b_mn = (BMODE == B_W_K) ? 0u : 1u;
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) |
+                                 ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        if (tl.nkb == 0) continue;
+        mbar_wait_cluster(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * TN);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          uint8_t *sa_ptr = tiles_smem + stage * STAGE_BYTES;
+          if (GK && kb == tl.nkb - 1) {
+            // bin tail: rows past the expert's bin belong to the next expert;
+            // zero them in both CTAs' tiles (peer via DSMEM) before the MMA.
+            const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+            if (valid < BK) {
+              zero_k_tail(sa_ptr, 4, valid, lane);
+              zero_k_tail_peer(smem_u32(sa_ptr), 1, 4, valid, lane);
+            }
+          }
+          if (RELAY) {
+            mbar_wait_cluster(smem_u32(&pready_bar[stage]), phase);
+            fence_proxy_async_smem();
+          }
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(sa_ptr);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              uint64_t ad, bd;
+              if (AM == A_MN) ad = sdesc(sa + k * 2048, 8192, 1024);
+              else ad = sdesc(sa + k * 32, 16, 1024);
+              if (BMODE == B_W_K) bd = sdesc(sb + k * 32, 16, 1024);
+              else bd = sdesc(sb + k * 2048, 8192, 1024);
+              umma_bf16_cg2(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            }
+            umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), 0x3);
+            if (kb == tl.nkb - 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    } else if (RELAY) {
+      // ===================== relay (peer CTA, gather mode): own stage landed -> leader =====================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(smem_u32(&pready_bar[stage]), 0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp < EPI_WARPS) {
+    // ===================== epilogue (own 128 rows) =====================
+    const int ew = warp;
+    const int q = warp & 3;
+    const int c_begin = (ew / 4) * EPI_COLS;
+    const int r = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const int64_t row = tl.m0 + HM * rank + r;
+      const bool valid = row < tl.m_end;
+      __nv_bfloat16 *orow = nullptr, *orow2 = nullptr;
+      const __nv_bfloat16 *arow = nullptr;
+      if (valid) {
+        int64_t dst;
+        if (GK) dst = (int64_t)tl.e * p.M + row;
+        else dst = p.grouped_out ? row : (int64_t)p.order[row];
+        orow = p.out + dst * p.N;
+        if (p.out2) orow2 = p.out2 + dst * p.N;
+        if (p.aux) arow = p.aux + dst * p.N;
+      }
+      const bool has_acc = tl.nkb > 0;
+      uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      const bool use_aux = (p.epi == SMOE_EPI_ACT_GRAD) && valid;
+      if (use_aux) {
+        const int64_t c0 = tl.n0 + c_begin;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (c0 + 8 * j < p.N) av[j] = __ldg(reinterpret_cast<const uint4 *>(arow + c0 + 8 * j));
+      }
+      if (has_acc) {
+        mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
+        tc_fence_after();
+      }
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
+#pragma unroll 1
+      for (int c = 0; c < EPI_COLS; c += 16) {
+        uint32_t v[16];
+        if (has_acc) {
+          tmem_ld16(tbase + c, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0u;
+        }
+        const int64_t col0 = tl.n0 + c_begin + c;
+        uint4 avn[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        if (use_aux && c + 16 < EPI_COLS) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (col0 + 16 + 8 * j < p.N) avn[j] = __ldg(reinterpret_cast<const uint4 *>(arow + col0 + 16 + 8 * j));
+        }
+        if (has_acc) tmem_ld_wait();
+        if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0);
+        av[0] = avn[0];
+        av[1] = avn[1];
+      }
+      if (has_acc) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(smem_u32(&tempty_bar[acc]));
+          else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (AM == A_GATHER) {
+    // ===================== cp.async gather of this CTA's 128 A rows =====================
+    const int g = threadIdx.x - 32 * EPI_WARPS;
+    const int chunk = g & 7;
+    const int rsub = g >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const int64_t m_half = tl.m0 + HM * rank;
+      const __nv_bfloat16 *src[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t row = min(m_half + j * 16 + rsub, tl.m_end - 1);
+        src[j] = p.x + (int64_t)(p.order[row] / p.fan_out) * p.K + chunk * 8;
+      }
+      for (int kb = 0; kb < tl.nkb; ++kb) {
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+        const int64_t col = (int64_t)kb * BK;
+        const bool ok = col + chunk * 8 < p.K;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rr = j * 16 + rsub;
+          cp_async16(sa + rr * 128 + ((chunk ^ (rr & 7)) << 4), ok ? (const void *)(src[j] + col) : (const void *)src[j],
+                     ok ? 16u : 0u);
+        }
+        cp_async_arrive_noinc(smem_u32(&lfull_bar[stage]));
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == WM) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// m-blocks per raster band for the grouped-K (weight-gradient) schedule: a
+// near-square block of the 74 concurrent cluster tiles (8 x ~9) maximises
+// panel sharing while each tile streams its long K (= bin) panels.
+static int group_m_k_setting() {
+  static int gm = -1;
+  if (gm < 0) {
+    const char *env = getenv("SMOE_GROUP_M_K");
+    gm = env ? atoi(env) : 8;
+    if (gm < 1) gm = 8;
+  }
+  return gm;
+}
+
+static size_t smem_bytes(int E) { return 1024 + STAGES * STAGE_BYTES + 8 * (3 * STAGES + 6) + 12 * (E + 1) + 64; }
+
+template <int AM, int BMODE, bool GK>
+static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, int64_t max_tiles, cudaStream_t st) {
+  auto kern = tc2_gemm_kernel<AM, BMODE, GK>;
+  size_t smem = smem_bytes(p.E);
+  static size_t configured = 0;
+  if (configured < smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return check_launch("tc2_gemm: smem attribute");
+    configured = smem;
+  }
+  int clusters = num_sms() / 2;
+  if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
+  tc2_gemm_kernel<AM, BMODE, GK><<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, p);
+  return check_launch("tc2_gemm");
+}
+
+int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                    const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout, int trans,
+                    int epi, int act, void *out, void *out2, const void *aux, cudaStream_t st) {
+  const int64_t d_in = trans ? w_cols : w_rows;
+  const int64_t d_out = trans ? w_rows : w_cols;
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[2] = {(uint64_t)d_in, (uint64_t)x_rows};
+    uint64_t strides[1] = {(uint64_t)d_in * 2};
+    uint32_t box[2] = {64, (uint32_t)HM};
+    if (!encode_map(&ta, x, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)w_cols, (uint64_t)w_rows, (uint64_t)E};
+    uint64_t strides[2] = {(uint64_t)w_cols * 2, (uint64_t)w_cols * w_rows * 2};
+    uint32_t box[3] = {64, trans ? (uint32_t)HN : 64u, 1};
+    if (!encode_map(&tb, w, 3, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(B) failed");
+  }
+  Params p{};
+  p.E = E;
+  p.M = n;
+  p.N = d_out;
+  p.K = d_in;
+  p.order = order;
+  p.offsets = offsets;
+  p.fan_out = fan_out;
+  p.grouped_out = gout;
+  p.epi = epi;
+  p.act = act;
+  p.out = (__nv_bfloat16 *)out;
+  p.out2 = (epi == SMOE_EPI_ACT) ? (__nv_bfloat16 *)out2 : nullptr;
+  p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
+  p.x = (const __nv_bfloat16 *)x;
+  p.group_m = (group_m_setting() + 1) / 2;
+  const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
+  if (gin) {
+    if (!trans) return launch<A_ROWS, B_W_MN, false>(ta, tb, p, max_tiles, st);
+    return launch<A_ROWS, B_W_K, false>(ta, tb, p, max_tiles, st);
+  }
+  if (!trans) return launch<A_GATHER, B_W_MN, false>(ta, tb, p, max_tiles, st);
+  return launch<A_GATHER, B_W_K, false>(ta, tb, p, max_tiles, st);
+}
+
+int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in, int64_t d_out,
+              void *dw, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  uint64_t rows = (uint64_t)(n > 0 ? n : 1);
+  {
+    uint64_t dims[2] = {(uint64_t)d_in, rows};
+    uint64_t strides[1] = {(uint64_t)d_in * 2};
+    uint32_t box[2] = {64, 64};
+    if (!encode_map(&ta, xg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Xg) failed");
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)d_out, rows};
+    uint64_t strides[1] = {(uint64_t)d_out * 2};
+    uint32_t box[2] = {64, 64};
+    if (!encode_map(&tb, yg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Yg) failed");
+  }
+  Params p{};
+  p.E = E;
+  p.M = d_in;
+  p.N = d_out;
+  p.K = 0;
+  p.offsets = offsets;
+  p.fan_out = 1;
+  p.grouped_out = 1;
+  p.epi = SMOE_EPI_NONE;
+  p.out = (__nv_bfloat16 *)dw;
+  p.group_m = group_m_k_setting();
+  const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
+  return launch<A_MN, B_ROWS_MN, true>(ta, tb, p, max_tiles, st);
+}
+
+}  // namespace tc2
+}  // namespace smoe

@@ -1,0 +1,348 @@
+// Shared PTX wrappers, parameters and tile schedule of the tcgen05 GEMM engines
+// (tc_gemm.cu: 1-CTA tiles; tc2_gemm.cu: 2-CTA cta_group::2 tiles).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace smoe {
+namespace tc {
+
+enum AMode { A_ROWS = 0, A_GATHER = 1, A_MN = 2 };
+enum BMode { B_W_MN = 0, B_W_K = 1, B_ROWS_MN = 2 };
+
+struct Params {
+  int E;
+  int64_t M;  // grouped-M: slots n;  grouped-K: d_in
+  int64_t N;  // d_out
+  int64_t K;  // grouped-M: d_in;     grouped-K: unused (bins)
+  const int32_t *order;
+  const int32_t *offsets;
+  int fan_out;
+  int grouped_out;
+  int epi;
+  int act;
+  __nv_bfloat16 *out;
+  __nv_bfloat16 *out2;
+  const __nv_bfloat16 *aux;
+  const __nv_bfloat16 *x;  // A_GATHER: the scattered input rows [x_rows, K]
+  int group_m;             // m-blocks per raster band
+};
+
+// ---- PTX wrappers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(const CUtensorMap *map, uint32_t bar, uint32_t dst, int col, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+// ---- cluster helpers (2-CTA pairs) ---------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(local_bar),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// commit prior cta_group::2 MMAs to the barrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_cg2_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"(mask)
+               : "memory");
+}
+
+// ---- tile schedule --------------------------------------------------------------
+struct Tile {
+  int e;
+  int64_t m0;     // first row of the tile (grouped-M: grouped position; grouped-K: d_in row)
+  int64_t m_end;  // rows >= m_end are masked
+  int64_t n0;
+  int64_t k0;     // grouped-K: first bin row
+  int64_t k_len;  // reduction length
+  int nkb;        // number of BK blocks
+};
+
+// Tile t -> (expert, m-block, n-block) with band rasterisation: group_m m-blocks
+// share each B panel while it is hot in L2.  s_start[e] = first tile of expert e.
+template <bool GK, int TM, int TN>
+__device__ __forceinline__ Tile decode_tile(int64_t t, const Params &p, const int64_t *s_start, const int32_t *s_off,
+                                            int64_t nN, int64_t mM) {
+  Tile tl;
+  int64_t e, local, mt;
+  if (!GK) {
+    int lo = 0, hi = p.E;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (s_start[mid] <= t) lo = mid; else hi = mid;
+    }
+    e = lo;
+    local = t - s_start[e];
+    mt = (s_off[e + 1] - s_off[e] + TM - 1) / TM;
+  } else {
+    e = t / (mM * nN);
+    local = t - e * (mM * nN);
+    mt = mM;
+  }
+  const int64_t band = local / (p.group_m * nN);
+  const int64_t rem = local - band * (p.group_m * nN);
+  const int64_t rows = min((int64_t)p.group_m, mt - band * p.group_m);
+  const int64_t mb = band * p.group_m + rem % rows;
+  const int64_t nb = rem / rows;
+  tl.e = (int)e;
+  tl.n0 = nb * TN;
+  if (!GK) {
+    tl.m0 = s_off[e] + mb * TM;
+    tl.m_end = s_off[e + 1];
+    tl.k0 = 0;
+    tl.k_len = p.K;
+  } else {
+    tl.m0 = mb * TM;
+    tl.m_end = p.M;
+    tl.k0 = s_off[e];
+    tl.k_len = s_off[e + 1] - s_off[e];
+  }
+  tl.nkb = (int)((tl.k_len + 63) / 64);
+  return tl;
+}
+
+// Zero K rows [valid, 64) of `boxes` consecutive 64-row x 128-B boxes (MN-major
+// tiles); 128-B rows are swizzle-invariant as a whole.  Called by one warp.
+__device__ __forceinline__ void zero_k_tail(uint8_t *base, int boxes, int valid, int lane) {
+  const int rows = 64 - valid;
+  const int chunks = rows * boxes * 8;
+  for (int c = lane; c < chunks; c += 32) {
+    const int box = c / (rows * 8);
+    const int rem = c - box * rows * 8;
+    const int r = valid + rem / 8;
+    const int q = rem % 8;
+    *reinterpret_cast<uint4 *>(base + box * 8192 + r * 128 + q * 16) = make_uint4(0, 0, 0, 0);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+}
+
+// Epilogue for one 16-column chunk of one accumulator row (fp32 in v[]).
+__device__ __forceinline__ void epilogue_chunk(const Params &p, const uint32_t (&v)[16], const uint4 (&av)[2],
+                                               __nv_bfloat16 *orow, __nv_bfloat16 *orow2, int64_t col0) {
+  float f[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+  uint32_t o1[8], o2[8];
+  if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_ONLY) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      __nv_bfloat162 pre = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      o1[i] = *reinterpret_cast<uint32_t *>(&pre);
+      float a0 = act_fwd_fast(p.act, __bfloat162float(pre.x));
+      float a1 = act_fwd_fast(p.act, __bfloat162float(pre.y));
+      o2[i] = pack_bf16(a0, a1);
+    }
+    if (p.epi == SMOE_EPI_ACT_ONLY) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o1[i] = o2[i];
+    }
+  } else if (p.epi == SMOE_EPI_ACT_GRAD) {
+    const __nv_bfloat162 *ah = reinterpret_cast<const __nv_bfloat162 *>(av);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float g0 = act_grad_fast(p.act, __bfloat162float(ah[i].x));
+      float g1 = act_grad_fast(p.act, __bfloat162float(ah[i].y));
+      o1[i] = pack_bf16(f[2 * i] * g0, f[2 * i + 1] * g1);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o1[i] = pack_bf16(f[2 * i], f[2 * i + 1]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    if (col0 + 8 * j >= p.N) break;
+    *reinterpret_cast<uint4 *>(orow + col0 + 8 * j) = make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+    if (p.epi == SMOE_EPI_ACT)
+      *reinterpret_cast<uint4 *>(orow2 + col0 + 8 * j) = make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
+  }
+}
+
+// ---- host helpers ----------------------------------------------------------------
+bool encode_map(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims, const uint64_t *strides,
+                const uint32_t *box);
+int group_m_setting();
+
+}  // namespace tc
+}  // namespace smoe
+
+namespace smoe {
+namespace tc {
+// ---- CTA-pair TMA: data lands in this CTA, bytes are counted on the LEADER's
+// barrier (same shared offset with the peer bit cleared), as the cta_group::2
+// TMA form requires.
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar & kPeerBitMask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_cg2(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar & kPeerBitMask)
+      : "memory");
+}
+// Zero K rows [valid, 64) of `boxes` MN-major 64-row boxes in the PEER CTA's
+// shared memory (DSMEM stores), then make them visible to the async proxy.
+__device__ __forceinline__ void zero_k_tail_peer(uint32_t local_base, uint32_t peer, int boxes, int valid, int lane) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_base), "r"(peer));
+  const int rows = 64 - valid;
+  const int chunks = rows * boxes * 8;
+  for (int c = lane; c < chunks; c += 32) {
+    const int box = c / (rows * 8);
+    const int rem = c - box * rows * 8;
+    const int r = valid + rem / 8;
+    const int q = rem % 8;
+    const uint32_t a = remote + box * 8192 + r * 128 + q * 16;
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+  __syncwarp();
+}
+}  // namespace tc
+}  // namespace smoe

@@ -28,7 +28,7 @@
 
 #include <cstdlib>
 
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace smoe {
 namespace tc {
@@ -40,205 +40,22 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 32;  // m-blocks per raster band (L2 reuse of B panels)
 
-enum AMode { A_ROWS = 0, A_GATHER = 1, A_MN = 2 };
-enum BMode { B_W_MN = 0, B_W_K = 1, B_ROWS_MN = 2 };
-
-struct Params {
-  int E;
-  int64_t M;  // grouped-M: slots n;  grouped-K: d_in
-  int64_t N;  // d_out
-  int64_t K;  // grouped-M: d_in;     grouped-K: unused (bins)
-  const int32_t *order;
-  const int32_t *offsets;
-  int fan_out;
-  int grouped_out;
-  int epi;
-  int act;
-  __nv_bfloat16 *out;
-  __nv_bfloat16 *out2;
-  const __nv_bfloat16 *aux;
-  const __nv_bfloat16 *x;  // A_GATHER: the scattered input rows [x_rows, K]
-  int group_m;             // m-blocks per raster band
-};
-
-// ---- PTX wrappers ------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_gather4(const CUtensorMap *map, uint32_t bar, uint32_t dst, int col, int r0, int r1,
-                                            int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-      "%6}], [%7];" ::"r"(dst),
-      "l"((uint64_t)map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
-}
-
-// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bit.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t *>(&h);
-}
-
-// ---- tile schedule --------------------------------------------------------------
-struct Tile {
-  int e;
-  int64_t m0;     // first row of the tile (grouped-M: grouped position; grouped-K: d_in row)
-  int64_t m_end;  // rows >= m_end are masked
-  int64_t n0;
-  int64_t k0;     // grouped-K: first bin row
-  int64_t k_len;  // reduction length
-  int nkb;        // number of BK blocks
-};
-
-template <bool GK>
-__device__ __forceinline__ Tile decode_tile(int64_t t, const Params &p, const int64_t *s_start, const int32_t *s_off,
-                                            int64_t nN, int64_t mM) {
-  Tile tl;
-  if (!GK) {
-    int lo = 0, hi = p.E;
-    while (hi - lo > 1) {
-      int mid = (lo + hi) >> 1;
-      if (s_start[mid] <= t) lo = mid; else hi = mid;
-    }
-    const int e = lo;
-    const int64_t local = t - s_start[e];
-    const int64_t cnt = s_off[e + 1] - s_off[e];
-    const int64_t mt = (cnt + BM - 1) / BM;
-    const int64_t band = local / (p.group_m * nN);
-    const int64_t rem = local - band * (p.group_m * nN);
-    const int64_t rows = min((int64_t)p.group_m, mt - band * p.group_m);
-    const int64_t mb = band * p.group_m + rem % rows;
-    const int64_t nb = rem / rows;
-    tl.e = e;
-    tl.m0 = s_off[e] + mb * BM;
-    tl.m_end = s_off[e + 1];
-    tl.n0 = nb * BN;
-    tl.k0 = 0;
-    tl.k_len = p.K;
-  } else {
-    const int64_t per = mM * nN;
-    const int e = (int)(t / per);
-    const int64_t local = t - (int64_t)e * per;
-    const int64_t band = local / (p.group_m * nN);
-    const int64_t rem = local - band * (p.group_m * nN);
-    const int64_t rows = min((int64_t)p.group_m, mM - band * p.group_m);
-    const int64_t mb = band * p.group_m + rem % rows;
-    const int64_t nb = rem / rows;
-    tl.e = e;
-    tl.m0 = mb * BM;
-    tl.m_end = p.M;
-    tl.n0 = nb * BN;
-    tl.k0 = s_off[e];
-    tl.k_len = s_off[e + 1] - s_off[e];
-  }
-  tl.nkb = (int)((tl.k_len + BK - 1) / BK);
-  return tl;
-}
-
 // ---- the kernel --------------------------------------------------------------------
 constexpr int EPI_WARPS = 8;                 // 2 warps per TMEM lane quarter, 128 columns each
 constexpr int GATHER_WARPS = 4;              // cp.async gather of A rows (A_GATHER only)
 constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
 __host__ __device__ constexpr int kernel_threads(int am) { return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0); }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
 
 template <int AM, int BMODE, bool GK>
 __global__ void __launch_bounds__(kernel_threads(AM), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, Params p) {
   constexpr int THREADS = kernel_threads(AM);
+  // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
+  // critical producer and MMA warps take the highest ids and never queue behind
+  // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
+  constexpr int WP = EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0);
+  constexpr int WM = WP + 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
@@ -258,7 +75,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
 
   // ---- one-time setup ----
   for (int i = threadIdx.x; i <= p.E; i += THREADS) s_off[i] = p.offsets[i];
-  if (warp == 0 && lane == 0) {
+  if (warp == WP && lane == 0) {
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
     for (int s = 0; s < STAGES; ++s) {
@@ -271,7 +88,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == WM) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -296,13 +113,13 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
   const uint32_t tmem_base = *s_tmem;
   const int64_t total = s_start[p.E];
 
-  if (warp == 0) {
+  if (warp == WP) {
     // ===================== TMA producer (B, and A unless gathered) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile tl = decode_tile<GK>(t, p, s_start, s_off, nN, mM);
+        const Tile tl = decode_tile<GK, BM, BN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           const uint32_t fb = smem_u32(&full_bar[stage]);
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
@@ -329,7 +146,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == WM) {
     // ===================== MMA issuer =====================
     constexpr uint32_t a_mn = (AM == A_MN) ? 1u : 0u;
     constexpr uint32_t b_mn = (BMODE == B_W_K) ? 0u : 1u;
@@ -340,7 +157,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile tl = decode_tile<GK>(t, p, s_start, s_off, nN, mM);
+      const Tile tl = decode_tile<GK, BM, BN>(t, p, s_start, s_off, nN, mM);
       if (tl.nkb == 0) continue;
       mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
       tc_fence_after();
@@ -387,16 +204,16 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp < 2 + EPI_WARPS) {
+  } else if (warp < EPI_WARPS) {
     // ===================== epilogue =====================
-    const int ew = warp - 2;
+    const int ew = warp;
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int c_begin = (ew / 4) * EPI_COLS;
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile tl = decode_tile<GK>(t, p, s_start, s_off, nN, mM);
+      const Tile tl = decode_tile<GK, BM, BN>(t, p, s_start, s_off, nN, mM);
       const int64_t row = tl.m0 + r;
       const bool valid = row < tl.m_end;
       __nv_bfloat16 *orow = nullptr, *orow2 = nullptr;
@@ -441,46 +258,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
             if (col0 + 16 + 8 * j < p.N) avn[j] = __ldg(reinterpret_cast<const uint4 *>(arow + col0 + 16 + 8 * j));
         }
         if (has_acc) tmem_ld_wait();
-        if (valid && col0 < p.N) {
-          float f[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
-          uint32_t o1[8], o2[8];
-          if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_ONLY) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 pre = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-              o1[i] = *reinterpret_cast<uint32_t *>(&pre);
-              float a0 = act_fwd(p.act, __bfloat162float(pre.x));
-              float a1 = act_fwd(p.act, __bfloat162float(pre.y));
-              o2[i] = pack_bf16(a0, a1);
-            }
-            if (p.epi == SMOE_EPI_ACT_ONLY) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) o1[i] = o2[i];
-            }
-          } else if (p.epi == SMOE_EPI_ACT_GRAD) {
-            const __nv_bfloat162 *ah = reinterpret_cast<const __nv_bfloat162 *>(av);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float g0 = act_grad(p.act, __bfloat162float(ah[i].x));
-              float g1 = act_grad(p.act, __bfloat162float(ah[i].y));
-              o1[i] = pack_bf16(f[2 * i] * g0, f[2 * i + 1] * g1);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o1[i] = pack_bf16(f[2 * i], f[2 * i + 1]);
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (col0 + 8 * j >= p.N) break;
-            *reinterpret_cast<uint4 *>(orow + col0 + 8 * j) =
-                make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
-            if (p.epi == SMOE_EPI_ACT)
-              *reinterpret_cast<uint4 *>(orow2 + col0 + 8 * j) =
-                  make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
-          }
-        }
+        if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0);
         av[0] = avn[0];
         av[1] = avn[1];
       }
@@ -498,13 +276,13 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
     // 128-B row slices (4 L1 wavefronts, not 32).  Chunks are written with the
     // SWIZZLE_128B pattern the UMMA descriptor expects: chunk c of tile row r
     // lands at chunk c ^ (r % 8).  Arrival is signalled when the copies land.
-    const int g = threadIdx.x - 32 * (2 + EPI_WARPS);
+    const int g = threadIdx.x - 32 * EPI_WARPS;
     const int chunk = g & 7;
     const int rsub = g >> 3;  // 0..15
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile tl = decode_tile<GK>(t, p, s_start, s_off, nN, mM);
+      const Tile tl = decode_tile<GK, BM, BN>(t, p, s_start, s_off, nN, mM);
       const __nv_bfloat16 *src[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -529,7 +307,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
   }
 
   __syncthreads();
-  if (warp == 1) {
+  if (warp == WM) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
@@ -555,7 +333,7 @@ static EncodeTiledFn get_encode() {
 }
 
 // dims/strides innermost first; strides (bytes) for dims 1.. ; box in elements.
-static bool encode(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims, const uint64_t *strides,
+bool encode_map(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims, const uint64_t *strides,
                    const uint32_t *box) {
   EncodeTiledFn fn = get_encode();
   if (!fn) return false;
@@ -567,7 +345,7 @@ static bool encode(CUtensorMap *m, const void *ptr, int rank, const uint64_t *di
   return r == CUDA_SUCCESS;
 }
 
-static int group_m() {
+int group_m_setting() {
   static int gm = -1;
   if (gm < 0) {
     const char *env = getenv("SMOE_GROUP_M");
@@ -611,6 +389,22 @@ bool tc_available() {
 
 static inline bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+namespace tc2 {
+int scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
+                    int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
+int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+}  // namespace tc2
+
+// 2 = CTA-pair kernels (tc2_gemm.cu, default), 1 = single-CTA kernels (this file).
+static int tc_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char *env = getenv("SMOE_TC_CTAS");
+    v = (env && atoi(env) == 1) ? 1 : 2;
+  }
+  return v;
+}
+
 bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out) {
   return d_in % 8 == 0 && d_out % 8 == 0 && d_in > 0 && d_out > 0 && al16(x) && al16(w) && al16(out) &&
          d_in < (1ll << 31) && d_out < (1ll << 31);
@@ -625,13 +419,16 @@ int tc_scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int6
   if (!tc_supports_s2s(d_in, d_out, x, w, out))
     return fail(SMOE_ENOTSUP, "tcgen05 scatter2scatter needs d_in, d_out multiples of 8 and 16-byte aligned buffers");
   if (E > 1024) return fail(SMOE_ENOTSUP, "tcgen05 path supports up to 1024 experts");
+  if (tc_ctas() == 2)
+    return tc2::scatter2scatter(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi,
+                                act, out, out2, aux, st);
   CUtensorMap ta, tb;
   // A: x [x_rows, d_in] row-major
   {
     uint64_t dims[2] = {(uint64_t)d_in, (uint64_t)x_rows};
     uint64_t strides[1] = {(uint64_t)d_in * 2};
     uint32_t box[2] = {64, gin ? (uint32_t)BM : 1u};
-    if (!encode(&ta, x, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    if (!encode_map(&ta, x, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(A) failed");
   }
   // B: W [E][w_rows][w_cols]
   {
@@ -640,7 +437,7 @@ int tc_scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int6
     uint32_t box[3];
     if (!trans) { box[0] = 64; box[1] = 64; box[2] = 1; }      // [K][N]: MN-major 64x64 boxes
     else { box[0] = 64; box[1] = (uint32_t)BN; box[2] = 1; }   // [N][K]: K-major 64 x 256 box
-    if (!encode(&tb, w, 3, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(B) failed");
+    if (!encode_map(&tb, w, 3, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(B) failed");
   }
   Params p{};
   p.E = E;
@@ -657,7 +454,7 @@ int tc_scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int6
   p.out2 = (epi == SMOE_EPI_ACT) ? (__nv_bfloat16 *)out2 : nullptr;
   p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
   p.x = (const __nv_bfloat16 *)x;
-  p.group_m = group_m();
+  p.group_m = group_m_setting();
   const int64_t max_tiles = ((n + BM - 1) / BM + E) * ((d_out + BN - 1) / BN);
   if (gin) {
     if (!trans) return launch<A_ROWS, B_W_MN, false>(ta, tb, p, max_tiles, st);
@@ -673,19 +470,20 @@ int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, 
   if (!(d_in % 8 == 0 && d_out % 8 == 0 && al16(xg) && al16(yg) && al16(dw)))
     return fail(SMOE_ENOTSUP, "tcgen05 group_xty needs d_in, d_out multiples of 8 and 16-byte aligned buffers");
   if (E > 1024) return fail(SMOE_ENOTSUP, "tcgen05 path supports up to 1024 experts");
+  if (tc_ctas() == 2) return tc2::group_xty(xg, yg, offsets, E, n, d_in, d_out, dw, st);
   CUtensorMap ta, tb;
   uint64_t rows = (uint64_t)(n > 0 ? n : 1);
   {
     uint64_t dims[2] = {(uint64_t)d_in, rows};
     uint64_t strides[1] = {(uint64_t)d_in * 2};
     uint32_t box[2] = {64, 64};
-    if (!encode(&ta, xg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Xg) failed");
+    if (!encode_map(&ta, xg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Xg) failed");
   }
   {
     uint64_t dims[2] = {(uint64_t)d_out, rows};
     uint64_t strides[1] = {(uint64_t)d_out * 2};
     uint32_t box[2] = {64, 64};
-    if (!encode(&tb, yg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Yg) failed");
+    if (!encode_map(&tb, yg, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Yg) failed");
   }
   Params p{};
   p.E = E;
@@ -699,7 +497,7 @@ int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, 
   p.epi = SMOE_EPI_NONE;
   p.act = 0;
   p.out = (__nv_bfloat16 *)dw;
-  p.group_m = group_m();
+  p.group_m = group_m_setting();
   const int64_t max_tiles = (int64_t)E * ((d_in + BM - 1) / BM) * ((d_out + BN - 1) / BN);
   return launch<A_MN, B_ROWS_MN, true>(ta, tb, p, max_tiles, st);
 }

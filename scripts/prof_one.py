@@ -25,6 +25,10 @@ for _ in range(3):
     elif which == "dh":
         sm.scatter2scatter(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, out=h2,
                            activation="gelu", act_grad_of=h)
+    elif which == "rows":
+        sm.scatter2scatter(xg, w, order, 1, sm.GROUPED_TO_GROUPED, out=h)
+    elif which == "xty":
+        sm.group_xty(h, xg, order)
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()
