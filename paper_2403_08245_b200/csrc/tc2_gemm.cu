@@ -13,9 +13,12 @@
 // pipe run at full rate (SURVEY.md §7 "2-CTA 256-row tiles").
 //
 // Synchronisation (mbarriers; "L" = leader only):
-//   lfull[s]  per CTA: its own TMA bytes (+128 cp.async gather arrivals) landed
-//   pready[s] L: the peer's stage s is ready (peer relay warp arrives remotely
-//             after optional K-tail zeroing)
+//   lfull[s]  per CTA: its own TMA bytes (+128 cp.async gather arrivals) landed.
+//             TMA-only modes count BOTH CTAs' bytes on the leader's lfull
+//             (cta_group::2 TMA).  Gather mode: the peer's relay warp waits on
+//             its own lfull and forwards a 16-byte DSMEM bulk copy whose
+//             complete_tx lands on the leader's lfull.
+//             Weight-gradient K tails are zeroed by the leader in both CTAs.
 //   empty[s]  per CTA: the leader's MMAs consumed stage s (multicast commit)
 //   tfull[a]  per CTA: accumulator a complete (multicast commit)
 //   tempty[a] L: both CTAs' epilogues drained accumulator a (16 arrivals)
@@ -26,7 +29,7 @@ namespace tc2 {
 
 using namespace smoe::tc;
 
-constexpr int TM = 256, TN = 256, BK = 64, STAGES = 6;
+constexpr int TM = 256, TN = 256, BK = 64, STAGES = 7;
 constexpr int HM = TM / 2, HN = TN / 2;  // per-CTA halves
 constexpr int A_BYTES = HM * BK * 2;     // 16 KB
 constexpr int B_BYTES = HN * BK * 2;     // 16 KB
@@ -34,6 +37,8 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARPS = 8;
 constexpr int GATHER_WARPS = 4;
+constexpr int G_RSTEP = GATHER_WARPS * 4;   // rows covered by one pass of all gather threads
+constexpr int G_RPT = 128 / G_RSTEP;        // rows per gather thread per k-block
 constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
 __host__ __device__ constexpr int kernel_threads(int am) {
   return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
@@ -48,17 +53,20 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
   constexpr int WP = EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0);
   constexpr int WM = WP + 1;
-  constexpr bool RELAY = (AM == A_GATHER);  // cp.async data cannot signal the leader's barrier
+  // cp.async data cannot signal the leader's barrier: gather mode relays it
+  constexpr bool RELAY = (AM == A_GATHER);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
   uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
   uint64_t *lfull_bar = bars;                    // [STAGES]
-  uint64_t *pready_bar = bars + STAGES;          // [STAGES]
+  // relay payload (16 B) + landing slot (16 B), 16-byte aligned inside bars[STAGES, 2*STAGES)
+  uint8_t *signal = (uint8_t *)((((uintptr_t)(bars + STAGES)) + 15) & ~(uintptr_t)15);
+  static_assert(STAGES * 8 >= 32 + 8, "relay slots need room");
   uint64_t *empty_bar = bars + 2 * STAGES;       // [STAGES]
   uint64_t *tfull_bar = bars + 3 * STAGES;       // [2]
   uint64_t *tempty_bar = bars + 3 * STAGES + 2;  // [2]
-  uint32_t *s_tmem = (uint32_t *)(bars + 3 * STAGES + 4);
+  uint32_t *s_tmem = (uint32_t *)(bars + 3 * STAGES + 4);  // bars[STAGES..2*STAGES) hold the relay signal
   int64_t *s_start = (int64_t *)(bars + 3 * STAGES + 6);  // [E+1]
   int32_t *s_off = (int32_t *)(s_start + p.E + 1);         // [E+1]
 
@@ -77,7 +85,6 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
     prefetch_tmap(&tma_b);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&lfull_bar[s]), AM == A_GATHER ? 1 + 32 * GATHER_WARPS : 1);
-      mbar_init(smem_u32(&pready_bar[s]), 1);
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -124,8 +131,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           const uint32_t sb = sa + A_BYTES;
           const int kk = kb * BK;
           if (RELAY) {
-            // gather mode: this CTA's bytes are counted locally and relayed
-            mbar_expect_tx(fb, B_BYTES);
+            // gather mode: this CTA's bytes are counted locally; the leader also
+            // expects the peer's 16-byte relay signal on the same barrier
+            mbar_expect_tx(fb, leader ? B_BYTES + 16 : B_BYTES);
             if (BMODE == B_W_MN) {
               tma_load_3d(&tma_b, fb, sb, n_half, kk, tl.e);
               tma_load_3d(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
@@ -190,10 +198,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
               zero_k_tail_peer(smem_u32(sa_ptr), 1, 4, valid, lane);
             }
           }
-          if (RELAY) {
-            mbar_wait_cluster(smem_u32(&pready_bar[stage]), phase);
-            fence_proxy_async_smem();
-          }
+          if (RELAY) fence_proxy_async_smem();
           tc_fence_after();
           if (lane == 0) {
             const uint32_t sa = smem_u32(sa_ptr);
@@ -225,7 +230,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(smem_u32(&pready_bar[stage]), 0);
+          // Signal the leader through the async proxy: a 16-byte DSMEM bulk copy
+          // whose complete_tx lands on the leader's lfull[stage].  Unlike a
+          // remote mbarrier.arrive it does not stall this thread.
+          if (lane == 0) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -302,31 +310,40 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
     const int g = threadIdx.x - 32 * EPI_WARPS;
     const int chunk = g & 7;
     const int rsub = g >> 3;
+    // Row indices of the NEXT tile are fetched while this tile streams, so no
+    // index-load latency bubble sits at tile boundaries.
+    auto load_rows = [&](int64_t t, int32_t (&dst)[G_RPT]) {
+      const Tile tn = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const int64_t mh = tn.m0 + HM * rank;
+#pragma unroll
+      for (int j = 0; j < G_RPT; ++j) dst[j] = __ldg(p.order + min(mh + j * G_RSTEP + rsub, tn.m_end - 1));
+    };
+    int32_t cur[G_RPT] = {}, nxt[G_RPT] = {};
+    if (cluster_id < total) load_rows(cluster_id, cur);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = cluster_id; t < total; t += num_clusters) {
       const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
-      const int64_t m_half = tl.m0 + HM * rank;
-      const __nv_bfloat16 *src[8];
+      if (t + num_clusters < total) load_rows(t + num_clusters, nxt);
+      const __nv_bfloat16 *src[G_RPT];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int64_t row = min(m_half + j * 16 + rsub, tl.m_end - 1);
-        src[j] = p.x + (int64_t)(p.order[row] / p.fan_out) * p.K + chunk * 8;
-      }
+      for (int j = 0; j < G_RPT; ++j) src[j] = p.x + (int64_t)(cur[j] / p.fan_out) * p.K + chunk * 8;
       for (int kb = 0; kb < tl.nkb; ++kb) {
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
         const int64_t col = (int64_t)kb * BK;
         const bool ok = col + chunk * 8 < p.K;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int rr = j * 16 + rsub;
+        for (int j = 0; j < G_RPT; ++j) {
+          const int rr = j * G_RSTEP + rsub;
           cp_async16(sa + rr * 128 + ((chunk ^ (rr & 7)) << 4), ok ? (const void *)(src[j] + col) : (const void *)src[j],
                      ok ? 16u : 0u);
         }
         cp_async_arrive_noinc(smem_u32(&lfull_bar[stage]));
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+#pragma unroll
+      for (int j = 0; j < G_RPT; ++j) cur[j] = nxt[j];
     }
   }
 

@@ -129,7 +129,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
@@ -343,6 +343,16 @@ __device__ __forceinline__ void zero_k_tail_peer(uint32_t local_base, uint32_t p
   }
   asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
   __syncwarp();
+}
+// 16-byte DSMEM bulk copy from this CTA to CTA 0 of the cluster; its
+// complete_tx is counted on CTA 0's barrier at offset `bar` (async proxy).
+__device__ __forceinline__ void bulk_signal_cta0(uint32_t dst_local, uint32_t src_local, uint32_t bar_local) {
+  uint32_t dst, bar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst) : "r"(dst_local));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(bar) : "r"(bar_local));
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(dst),
+               "r"(src_local), "r"(bar)
+               : "memory");
 }
 }  // namespace tc
 }  // namespace smoe

@@ -14,12 +14,12 @@ def main(path, only_ours=True):
         if len(r) <= vi:
             continue
         name = r[ki]
-        if only_ours and "smoe" not in name and "tc_gemm" not in name:
+        if only_ours and "smoe" not in name and "gemm_kernel" not in name:
             continue
         short = re.sub(r"\(.*", "", name)
-        m = re.search(r"tc_gemm_kernel<(\d+), (\d+), (\w+)>", name)
+        m = re.search(r"(tc2?)_gemm_kernel<(\d+), (\d+), (\w+)>", name)
         if m:
-            short = f"tc_gemm<A{m.group(1)},B{m.group(2)},GK={m.group(3)}>"
+            short = f"{m.group(1)}_gemm<A{m.group(2)},B{m.group(3)},GK={m.group(4)}>"
         out.append((int(r[ii]), short, float(r[vi].replace(",", "")) / 1e3))
     for i, s, us in out:
         print(f"{i:5d} {us:10.1f} us  {s}")

@@ -25,8 +25,17 @@ for _ in range(3):
     elif which == "dh":
         sm.scatter2scatter(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, out=h2,
                            activation="gelu", act_grad_of=h)
+    elif which == "gather":
+        sm.scatter2scatter(x, w, order, k, sm.SCATTERED_TO_GROUPED, out=h)
+    elif which == "dhnone":
+        sm.scatter2scatter(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, out=h2)
+    elif which == "dx":
+        sm.scatter2scatter(h, w, order, 1, sm.GROUPED_TO_SCATTERED, transpose_w=True, out=xg)
     elif which == "rows":
         sm.scatter2scatter(xg, w, order, 1, sm.GROUPED_TO_GROUPED, out=h)
+    elif which == "xtyboth":
+        sm.group_xty(h, xg, order)
+        sm.group_xty(xg, h, order)
     elif which == "xty":
         sm.group_xty(h, xg, order)
     elif which == "l2":
