@@ -179,17 +179,30 @@ def run_ours(args, rank, world, local_rank):
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = (torch.rand((T, d), generator=g, device=dev) * 2 - 1).to(dtype)
     dy = (torch.rand((T, d), generator=g, device=dev) * 2 - 1).to(dtype)
-    cfg = sm.SmoeMlpConfig(d_model=d, d_expert=de, num_experts=E, k=k)
+    if world > 1 and E % world:
+        raise SystemExit(f"EP needs num_experts ({E}) divisible by the number of GPUs ({world})")
+    e_local = E // world if world > 1 else E
+    cfg = sm.SmoeMlpConfig(d_model=d, d_expert=de, num_experts=e_local, k=min(k, e_local))
     w1, w2 = sm.init_smoe_mlp_weights(cfg, 101 + rank, dtype=dtype, device=dev, source="device")
     wg = (torch.rand((d, E), generator=g, device=dev) * 2 - 1) / (d ** 0.5)
     routing = sm.topk_select(sm.gate_forward(x.float(), wg), k)
     torch.cuda.synchronize()
 
-    def step(xx, dyy, rt):
-        order = sm.compute_grouped_order(rt)
-        y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
-        grads = sm.smoe_mlp_backward(ctx, dyy)
-        return y, grads
+    if world > 1:
+        # expert parallelism: this rank owns experts [rank*E/G, (rank+1)*E/G)
+        from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
+        ep = ExpertParallelSmoeMlp(w1, w2, E)
+
+        def step(xx, dyy, rt):
+            y, ctx = ep.forward(xx, rt)
+            grads = ep.backward(ctx, dyy)
+            return y, grads
+    else:
+        def step(xx, dyy, rt):
+            order = sm.compute_grouped_order(rt)
+            y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
+            grads = sm.smoe_mlp_backward(ctx, dyy)
+            return y, grads
 
     def barrier():
         if world > 1:
@@ -262,14 +275,21 @@ def run_ours(args, rank, world, local_rank):
         ms_e2e = float(t)
 
     # ---- roofline: dominant kernel (layer-1 forward grouped GEMM) alone ----
-    order = sm.compute_grouped_order(routing)
-    n = T * k
+    if world > 1:
+        # this rank's local experts only (the EP shard)
+        kk = min(k, e_local)
+        rt_local = sm.topk_select(torch.softmax(torch.randn(T, e_local, device=dev, generator=g), 1), kk)
+        order = sm.compute_grouped_order(rt_local)
+    else:
+        kk = k
+        order = sm.compute_grouped_order(routing)
+    n = T * kk
     h_pre = torch.empty((n, de), dtype=dtype, device=dev)
     h = torch.empty_like(h_pre)
     reps = 10
 
     def l1():
-        sm.scatter2scatter(x, w1, order, k, sm.SCATTERED_TO_GROUPED, out=h_pre, activation="gelu", act_out=h)
+        sm.scatter2scatter(x, w1, order, kk, sm.SCATTERED_TO_GROUPED, out=h_pre, activation="gelu", act_out=h)
 
     for _ in range(2):
         l1()
@@ -310,7 +330,8 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, softmax top-k routing)",
             "config": {"workload": desc, "global_batch": T * world, "seq_len": None,
-                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "parallelism": f"ep{world} (experts sharded, NCCL all-to-all-v dispatch/combine)" if world > 1
+                       else "single GPU",
                        "l2": "inputs larger than L2 (W1+W2 1.9 GB, H 1.9 GB); no flush",
                        "engine": sm.get_engine(), "timed": "flatten_and_sort + smoe_mlp_forward + smoe_mlp_backward"},
             "tflops_per_gpu": tflops_per_gpu,
@@ -345,8 +366,6 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if args.ref_tokens == 128:
-            args.ref_tokens = 64
         run_reference(args, rank, world)
         return
 
