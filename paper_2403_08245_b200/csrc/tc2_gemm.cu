@@ -38,7 +38,12 @@ constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARPS = 8;
 constexpr int GATHER_WARPS = 4;
 constexpr int G_RSTEP = GATHER_WARPS * 4;   // rows covered by one pass of all gather threads
-constexpr int G_RPT = 128 / G_RSTEP;        // rows per gather thread per k-block
+// Gather mode: A rows fetched by TMA tile::gather4 from the producer lanes
+// instead of cp.async.  Measured at C1 layer 1 (base clock, tensor-pipe active):
+// 0 rows 72 %, 32 rows 57 % — each gather4 costs far more TMA issue time than
+// the 512 B it moves, so the cp.async warps carry all rows.
+constexpr int TG_ROWS = 0;
+constexpr int G_RPT = (128 - TG_ROWS) / G_RSTEP;  // rows per cp.async gather thread per k-block
 constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
 __host__ __device__ constexpr int kernel_threads(int am) {
   return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
@@ -117,23 +122,31 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
 
   if (warp == WP) {
     // ===================== TMA producer (own halves of A and B) =====================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
-        const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
-        const int n_half = (int)(tl.n0 + HN * rank);
-        for (int kb = 0; kb < tl.nkb; ++kb) {
-          const uint32_t fb = smem_u32(&lfull_bar[stage]);
+    // Gather mode: lanes 0..TG_ROWS/4-1 also fetch the first TG_ROWS A rows with
+    // TMA tile::gather4 (4 rows per instruction), offloading the cp.async warps.
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
+      const int n_half = (int)(tl.n0 + HN * rank);
+      int gr[4] = {0, 0, 0, 0};
+      const bool g4_lane = (AM == A_GATHER) && lane < TG_ROWS / 4;
+      if (g4_lane) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gr[j] = __ldg(p.order + min((int64_t)m_half + 4 * lane + j, tl.m_end - 1)) / p.fan_out;
+      }
+      for (int kb = 0; kb < tl.nkb; ++kb) {
+        const uint32_t fb = smem_u32(&lfull_bar[stage]);
+        const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+        const int kk = kb * BK;
+        if (lane == 0) {
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-          const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
-          const int kk = kb * BK;
           if (RELAY) {
             // gather mode: this CTA's bytes are counted locally; the leader also
             // expects the peer's 16-byte relay signal on the same barrier
-            mbar_expect_tx(fb, leader ? B_BYTES + 16 : B_BYTES);
+            mbar_expect_tx(fb, B_BYTES + TG_ROWS * 128 + (leader ? 16 : 0));
             if (BMODE == B_W_MN) {
               tma_load_3d(&tma_b, fb, sb, n_half, kk, tl.e);
               tma_load_3d(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
@@ -159,11 +172,15 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
               tma_load_2d_cg2(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
             }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (g4_lane) tma_gather4(&tma_a, fb, sa + lane * 512, kk, gr[0], gr[1], gr[2], gr[3]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      // Producer tail: wait until every stage's last fill was consumed, so no
-      // multicast commit can still be in flight to this CTA when it exits.
+    }
+    // Producer tail: wait until every stage's last fill was consumed, so no
+    // multicast commit can still be in flight to this CTA when it exits.
+    if (lane == 0) {
       for (int i = 0; i < STAGES; ++i) {
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -180,14 +197,20 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      // p.timing: per-cluster cycle counters of the issue loop (SMOE_TC_TIMING=1, debug)
+      long long c_start = clock64(), c_tempty = 0, c_lfull = 0;
       for (int64_t t = cluster_id; t < total; t += num_clusters) {
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         if (tl.nkb == 0) continue;
+        long long c0 = p.timing ? clock64() : 0;
         mbar_wait_cluster(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+        if (p.timing) c_tempty += clock64() - c0;
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * TN);
         for (int kb = 0; kb < tl.nkb; ++kb) {
+          long long c1 = p.timing ? clock64() : 0;
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          if (p.timing) c_lfull += clock64() - c1;
           uint8_t *sa_ptr = tiles_smem + stage * STAGE_BYTES;
           if (GK && kb == tl.nkb - 1) {
             // bin tail: rows past the expert's bin belong to the next expert;
@@ -220,6 +243,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      if (p.timing && lane == 0 && cluster_id < 4)
+        printf("tc2 timing cluster %d: total %lld cyc, wait tempty %lld (%.1f%%), wait lfull %lld (%.1f%%)\n",
+               (int)cluster_id, clock64() - c_start, c_tempty, 100.0 * c_tempty / (clock64() - c_start), c_lfull,
+               100.0 * c_lfull / (clock64() - c_start));
     } else if (RELAY) {
       // ===================== relay (peer CTA, gather mode): own stage landed -> leader =====================
       int stage = 0;
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       const Tile tn = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
       const int64_t mh = tn.m0 + HM * rank;
 #pragma unroll
-      for (int j = 0; j < G_RPT; ++j) dst[j] = __ldg(p.order + min(mh + j * G_RSTEP + rsub, tn.m_end - 1));
+      for (int j = 0; j < G_RPT; ++j) dst[j] = __ldg(p.order + min(mh + TG_ROWS + j * G_RSTEP + rsub, tn.m_end - 1));
     };
     int32_t cur[G_RPT] = {}, nxt[G_RPT] = {};
     if (cluster_id < total) load_rows(cluster_id, cur);
@@ -335,7 +362,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         const bool ok = col + chunk * 8 < p.K;
 #pragma unroll
         for (int j = 0; j < G_RPT; ++j) {
-          const int rr = j * G_RSTEP + rsub;
+          const int rr = TG_ROWS + j * G_RSTEP + rsub;
           cp_async16(sa + rr * 128 + ((chunk ^ (rr & 7)) << 4), ok ? (const void *)(src[j] + col) : (const void *)src[j],
                      ok ? 16u : 0u);
         }
@@ -396,7 +423,7 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   {
     uint64_t dims[2] = {(uint64_t)d_in, (uint64_t)x_rows};
     uint64_t strides[1] = {(uint64_t)d_in * 2};
-    uint32_t box[2] = {64, (uint32_t)HM};
+    uint32_t box[2] = {64, gin ? (uint32_t)HM : 1u};  // gather mode: tile::gather4 rows
     if (!encode_map(&ta, x, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(A) failed");
   }
   {
@@ -421,6 +448,7 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
   p.x = (const __nv_bfloat16 *)x;
   p.group_m = (group_m_setting() + 1) / 2;
+  p.timing = getenv("SMOE_TC_TIMING") != nullptr;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
   if (gin) {
     if (!trans) return launch<A_ROWS, B_W_MN, false>(ta, tb, p, max_tiles, st);
@@ -457,6 +485,7 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   p.epi = SMOE_EPI_NONE;
   p.out = (__nv_bfloat16 *)dw;
   p.group_m = group_m_k_setting();
+  p.timing = getenv("SMOE_TC_TIMING") != nullptr;
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
   return launch<A_MN, B_ROWS_MN, true>(ta, tb, p, max_tiles, st);
 }

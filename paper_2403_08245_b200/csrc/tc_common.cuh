@@ -28,6 +28,7 @@ struct Params {
   const __nv_bfloat16 *aux;
   const __nv_bfloat16 *x;  // A_GATHER: the scattered input rows [x_rows, K]
   int group_m;             // m-blocks per raster band
+  int timing;              // debug: print issue-loop wait counters (SMOE_TC_TIMING)
 };
 
 // ---- PTX wrappers ------------------------------------------------------------

@@ -6,8 +6,9 @@
 //   scatter2scatter (kernels.py:143-220), "grouped-M" schedule:
 //     tiles = sum_e ceil(count_e / 128) x ceil(d_out / 256); K = d_in
 //     A rows: grouped (TMA 2D tile) or gathered straight from the scattered
-//             input with TMA tile::gather4 (row = order[i] / fan_out) — no
-//             padded or grouped copy of X is ever made;
+//             input by 4 cp.async warps (row = order[i] / fan_out), written in
+//             the 128-B swizzle pattern — no padded or grouped copy of X is
+//             ever made (TMA tile::gather4 measured 3x slower: 32 issues/stage);
 //     B     : W[e] as a 3D tensor map, MN-major (forward) or K-major (W^T for
 //             the input gradients, never materialised transposed);
 //     epilogue: TMEM -> registers -> (pre, act(pre)) | act | acc*act'(aux) ->
@@ -17,10 +18,13 @@
 //     A = Xg^T and B = Yg both MN-major; bin-tail rows are zeroed in shared
 //     memory before the last MMA; empty bins write zeros (no MMA).
 //
-// Roles (192 threads, one CTA per SM, grid = #SMs, static round-robin tiles):
-//   warp 0      TMA producer (all 32 lanes issue gather4 in gather mode)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue (warp w reads TMEM lanes 32*(w%4) .. +31)
+// This single-CTA engine (128 x 256 tiles) is kept as the SMOE_TC_CTAS=1
+// alternative and A/B reference; the default bf16 engine is the CTA-pair
+// kernel of tc2_gemm.cu.
+// Roles (one CTA per SM, grid = #SMs, static round-robin tiles):
+//   warps 0..7   epilogue (warp w reads TMEM lanes 32*(w%4) .. +31, column half w/4)
+//   warps 8..11  cp.async gather of A rows (gather mode only)
+//   next warp    TMA producer;  last warp  TMEM allocator + tcgen05.mma issuer
 // Pipelines: 4-stage smem ring (full/empty mbarriers, 48 KB per stage) and a
 // 2-stage TMEM accumulator ring (2 x 256 fp32 columns = all 512 columns), so the
 // epilogue of tile t overlaps the MMAs of tile t+1.

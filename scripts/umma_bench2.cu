@@ -1,9 +1,8 @@
-// Microbenchmark: tcgen05.mma throughput vs operand major-ness (K-major / MN-major).
-// One CTA per SM issues back-to-back M=128 N=256 K=16 bf16 MMAs from static
-// shared-memory tiles (SWIZZLE_128B descriptors, same as the product kernels)
-// and reports cycles per MMA.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
-#include <cstdio>
+// Microbenchmark: CTA-pair tcgen05.mma.cta_group::2 (M=256 N=256 K=16) issue rate by
+// operand major-ness, from static shared-memory tiles (no TMA).  One cluster of 2
+// CTAs per TPC.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -17,28 +16,31 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;
 }
 
-template <int A_MN, int B_MN, int SMEM_NOISE = 0>
-__global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long *out) {
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) bench(int iters, unsigned long long *out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem;
-  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) ((uint4 *)smem)[i] = make_uint4(0, 0, 0, 0);
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x) ((uint4 *)smem)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (threadIdx.x < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)A_MN << 15) | ((uint32_t)B_MN << 16) |
-                         ((256u >> 3) << 17) | ((128u >> 4) << 24);
-  if (threadIdx.x == 0) {
+                         ((256u >> 3) << 17) | ((256u >> 4) << 24);
+  if (rank == 0 && threadIdx.x == 0) {
     const uint32_t sa = smem_u32(smem), sb = sa + 16384;
     unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -49,47 +51,40 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long *o
         uint32_t acc = (it | k) != 0;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
             "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
       }
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(&bar)),
+                 "h"((uint16_t)1));
     asm volatile(
         "{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(
             smem_u32(&bar)));
     unsigned long long t1 = clock64();
-    out[blockIdx.x] = t1 - t0;
-    if (SMEM_NOISE) ((volatile uint32_t *)(smem + 49152))[0] = 1u;  // stop flag for the noise warps
-  } else if (SMEM_NOISE && threadIdx.x >= 32) {
-    // generic-proxy 16-byte stores into a separate 16 KB region (like cp.async / LDGSTS landing)
-    volatile uint32_t *flag = (volatile uint32_t *)(smem + 49152);
-    uint4 *dst = (uint4 *)(smem + 32768 + 16384);
-    int i = threadIdx.x;
-    while (*flag == 0u) {
-      dst[(i * 7) & 1023] = make_uint4(i, i, i, i);
-      i += 96;
-    }
+    out[blockIdx.x / 2] = t1 - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-template <int A, int B, int NOISE = 0>
+template <int A, int B>
 void run(const char *name, int sms) {
   unsigned long long *d, h[256];
   cudaMalloc(&d, sizeof(h));
-  auto k = bench<A, B, NOISE>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  auto k = bench<A, B>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 34 * 1024);
   const int iters = 4096;
-  k<<<sms, 128, 66 * 1024>>>(iters, d);
-  k<<<sms, 128, 66 * 1024>>>(iters, d);
+  k<<<sms, 128, 34 * 1024>>>(iters, d);
+  k<<<sms, 128, 34 * 1024>>>(iters, d);
   cudaDeviceSynchronize();
-  cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h, d, sizeof(unsigned long long) * (sms / 2), cudaMemcpyDeviceToHost);
   double avg = 0;
-  for (int i = 0; i < sms; ++i) avg += h[i];
-  avg /= sms;
-  printf("%-22s cycles/MMA = %.1f  (ideal 128 for M128 N256 K16)  err=%s\n", name, avg / (iters * 4.0),
+  for (int i = 0; i < sms / 2; ++i) avg += h[i];
+  avg /= (sms / 2);
+  printf("cg2 %-22s cycles/MMA = %.1f  (ideal 128 for M256 N256 K16 per pair)  err=%s\n", name, avg / (iters * 4.0),
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -101,7 +96,5 @@ int main() {
   run<0, 1>("A K-major, B MN-major", sms);
   run<1, 0>("A MN-major, B K-major", sms);
   run<1, 1>("A MN-major, B MN-major", sms);
-  run<0, 1, 1>("K/MN + smem st noise", sms);
-  run<1, 1, 1>("MN/MN + smem st noise", sms);
   return 0;
 }
