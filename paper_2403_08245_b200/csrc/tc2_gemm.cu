@@ -448,7 +448,7 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
   p.x = (const __nv_bfloat16 *)x;
   p.group_m = (group_m_setting() + 1) / 2;
-  p.timing = getenv("SMOE_TC_TIMING") != nullptr;
+  p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
   if (gin) {
     if (!trans) return launch<A_ROWS, B_W_MN, false>(ta, tb, p, max_tiles, st);
@@ -485,7 +485,7 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   p.epi = SMOE_EPI_NONE;
   p.out = (__nv_bfloat16 *)dw;
   p.group_m = group_m_k_setting();
-  p.timing = getenv("SMOE_TC_TIMING") != nullptr;
+  p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
   return launch<A_MN, B_ROWS_MN, true>(ta, tb, p, max_tiles, st);
 }
