@@ -83,6 +83,23 @@ int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
                     size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Router, the step in front of the sort.
+ * smoe_router_topk replaces softmax_rows + topk_select (router.py:126-151) and,
+ * with apply_softmax, gate_forward's softmax (router.py:119-123; the gate GEMM
+ * itself is a plain library matmul):
+ *   in        [T, E] float32 logits (apply_softmax=1) or gate probabilities
+ *   gate_out  [T, E] float32 softmax output, or NULL
+ *   expert_idx[T, k] int64: k largest gates, ties -> lower expert id (k <= 8)
+ *   p         [T, k] float32: selected gates, renormalised in float64 if asked
+ * smoe_router_backward replaces gate_backward (router.py:167-188):
+ *   dlogits [T, E] float32 from grad_p [T, k] through renormalisation + softmax.
+ */
+int smoe_router_topk(const float *in, int64_t T, int32_t num_experts, int32_t k, int32_t apply_softmax,
+                     int32_t renormalize, float *gate_out, int64_t *expert_idx, float *p, void *stream);
+int smoe_router_backward(const float *gate, const int64_t *expert_idx, const float *grad_p, int64_t T,
+                         int32_t num_experts, int32_t k, int32_t renormalized, float *dlogits, void *stream);
+
+/* ---------------------------------------------------------------------------
  * scatter2scatter (kernels.py:143-220): for each grouped position i in bin e,
  *   src = grouped_in ? i : order[i] / fan_out
  *   dst = grouped_out ? i : order[i]

@@ -60,6 +60,29 @@ def topk_routing(gate: np.ndarray, k: int):
     return idx, p
 
 
+def softmax_rows(logits: np.ndarray) -> np.ndarray:
+    """Row softmax in float64, stored in the input dtype (router.py:126-134)."""
+    z = logits.astype(F64)
+    z = z - z.max(axis=1, keepdims=True)
+    e = np.exp(z)
+    return (e / e.sum(axis=1, keepdims=True)).astype(logits.dtype)
+
+
+def gate_backward(gate, idx, grad_p, renormalized=True):
+    """d logits from d p through renormalisation, selection and softmax (router.py:167-188)."""
+    g = gate.astype(F64)
+    dp = grad_p.astype(F64)
+    gsel = np.take_along_axis(g, idx, axis=1)
+    if renormalized:
+        s = gsel.sum(axis=1, keepdims=True)
+        dgsel = (dp - (dp * (gsel / s)).sum(axis=1, keepdims=True)) / s
+    else:
+        dgsel = dp
+    dg = np.zeros_like(g)
+    np.put_along_axis(dg, idx, dgsel, axis=1)
+    return (g * (dg - (dg * g).sum(axis=1, keepdims=True))).astype(gate.dtype)
+
+
 def gate_probs(x: np.ndarray, w_g: np.ndarray) -> np.ndarray:
     """softmax(x @ w_g) in float64, stored float32 (router.py:119-134)."""
     z = x.astype(F64) @ w_g.astype(F64)

@@ -35,6 +35,8 @@ int activation(const void *, int64_t, int, int, int, void *, cudaStream_t);
 int simt_scatter2scatter(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int simt_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int, void *, cudaStream_t);
 int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, const float *, int, int, int, float *, void *, cudaStream_t);
+int router_topk(const float *, int64_t, int, int, int, int, float *, int64_t *, float *, cudaStream_t);
+int router_backward(const float *, const int64_t *, const float *, int64_t, int, int, int, float *, cudaStream_t);
 bool tc_available();
 bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out);
 int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
@@ -73,6 +75,20 @@ int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
   REQUIRE(expert_offsets, SMOE_EINVAL, "route_sort: null expert_offsets");
   return route_sort(expert_idx, n, num_experts, sorted_scattered_idxs, sorted_expert_idxs,
                     expert_offsets, inverse, workspace, workspace_bytes, S(stream));
+}
+
+int smoe_router_topk(const float *in, int64_t T, int32_t num_experts, int32_t k, int32_t apply_softmax,
+                     int32_t renormalize, float *gate_out, int64_t *expert_idx, float *p, void *stream) {
+  REQUIRE(T >= 0, SMOE_EINVAL, "router_topk: T must be >= 0");
+  REQUIRE(T == 0 || (in && expert_idx && p), SMOE_EINVAL, "router_topk: null pointer");
+  return router_topk(in, T, num_experts, k, apply_softmax, renormalize, gate_out, expert_idx, p, S(stream));
+}
+
+int smoe_router_backward(const float *gate, const int64_t *expert_idx, const float *grad_p, int64_t T,
+                         int32_t num_experts, int32_t k, int32_t renormalized, float *dlogits, void *stream) {
+  REQUIRE(T >= 0, SMOE_EINVAL, "router_backward: T must be >= 0");
+  REQUIRE(T == 0 || (gate && expert_idx && grad_p && dlogits), SMOE_EINVAL, "router_backward: null pointer");
+  return router_backward(gate, expert_idx, grad_p, T, num_experts, k, renormalized, dlogits, S(stream));
 }
 
 int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t num_experts,

@@ -207,11 +207,47 @@ def softmax_rows(logits: torch.Tensor) -> torch.Tensor:
     return _softmax_rows64(logits.to(torch.float64)).to(logits.dtype)
 
 
+def _router_kernel(inp: torch.Tensor, k: int, renormalize: bool, apply_softmax: bool):
+    """csrc/router.cu: (gate, expert_idx, p) for a CUDA [T, E] float32 input."""
+    t, e = inp.shape
+    inp = inp.to(torch.float32).contiguous()
+    idx = torch.empty((t, k), dtype=torch.int64, device=inp.device)
+    p = torch.empty((t, k), dtype=torch.float32, device=inp.device)
+    gate = torch.empty_like(inp) if apply_softmax else inp
+    st = _lib.load().smoe_router_topk(inp.data_ptr(), t, e, k, int(apply_softmax), int(renormalize),
+                                      gate.data_ptr() if apply_softmax else None, idx.data_ptr(), p.data_ptr(),
+                                      _stream_ptr(inp.device))
+    _lib.check(st, "router_topk")
+    return gate, idx, p
+
+
+def route(logits: torch.Tensor, k: int, renormalize: bool = True) -> RoutingResult:
+    """Fused softmax + stable top-k + renormalisation of float32 logits (one kernel).
+
+    Equivalent to topk_select(softmax_rows(logits), k) (router.py:126-151) with
+    the softmax evaluated in float64 and rounded once, as the reference does.
+    """
+    t, e = logits.shape
+    if not 1 <= k <= e:
+        raise ValueError(f"k must be in [1, E]; got k={k}, E={e}")
+    if not logits.is_cuda:
+        return topk_select(softmax_rows(logits.to(torch.float32)), k, renormalize)
+    gate, idx, p = _router_kernel(logits, k, renormalize, apply_softmax=True)
+    return RoutingResult(expert_idx=idx, p=p, gate_full=gate, renormalized=renormalize, validate=False)
+
+
 def topk_select(gate: torch.Tensor, k: int, renormalize: bool = True) -> RoutingResult:
-    """Each row's k largest gates; ties toward the lower expert id (router.py:137-151)."""
+    """Each row's k largest gates; ties toward the lower expert id (router.py:137-151).
+
+    CUDA inputs run the router kernel (csrc/router.cu, k <= 8); CPU tensors use
+    torch ops (host-side utilities and tests).
+    """
     t, e = gate.shape
     if not 1 <= k <= e:
         raise ValueError(f"k must be in [1, E]; got k={k}, E={e}")
+    if gate.is_cuda and k <= 8:
+        _, idx, p = _router_kernel(gate, k, renormalize, apply_softmax=False)
+        return RoutingResult(expert_idx=idx, p=p, gate_full=gate, renormalized=renormalize, validate=False)
     order = torch.sort(-gate, dim=1, stable=True).indices
     idx = order[:, :k].to(torch.int64).contiguous()
     sel = torch.gather(gate, 1, idx)
@@ -224,8 +260,18 @@ def topk_select(gate: torch.Tensor, k: int, renormalize: bool = True) -> Routing
 
 
 def gate_backward(routing: RoutingResult, grad_p: torch.Tensor) -> torch.Tensor:
-    """Gradient wrt gate logits given dL/dp (router.py:167-188)."""
+    """Gradient wrt gate logits given dL/dp (router.py:167-188); router kernel on CUDA."""
     require_dims(tuple(grad_p.shape) == tuple(routing.p.shape), "grad_p vs p", grad_p.shape, routing.p.shape)
+    if routing.gate_full.is_cuda:
+        t, e = routing.gate_full.shape
+        gate = routing.gate_full.to(torch.float32).contiguous()
+        gp = grad_p.to(torch.float32).contiguous()
+        idx = routing.expert_idx.to(torch.int64).contiguous()
+        dz = torch.empty_like(gate)
+        st = _lib.load().smoe_router_backward(gate.data_ptr(), idx.data_ptr(), gp.data_ptr(), t, e, routing.k,
+                                              int(routing.renormalized), dz.data_ptr(), _stream_ptr(gate.device))
+        _lib.check(st, "router_backward")
+        return dz.to(routing.gate_full.dtype)
     g = routing.gate_full.to(torch.float64)
     dp = grad_p.to(torch.float64)
     sel = routing.expert_idx

@@ -221,7 +221,38 @@ def momha_fixtures():
                         seq_len=np.int64(seq_len))
 
 
+def gate_fixtures():
+    """gate_forward / softmax_rows / topk_select / gate_backward (router.py:119-188)."""
+    out = {}
+    rng = np.random.default_rng(11)
+    j = 0
+    for t, d, e, k, renorm in [(37, 16, 8, 2, True), (64, 32, 64, 8, True), (20, 8, 5, 3, False), (9, 4, 40, 4, True)]:
+        x = Matrix(rng.uniform(-1, 1, (t, d)).astype(np.float32))
+        wg = Matrix((rng.uniform(-1, 1, (d, e)) / np.sqrt(d)).astype(np.float32))
+        gate = sm.gate_forward(x, wg)
+        r = sm.topk_select(gate, k, renormalize=renorm)
+        gp = rng.uniform(-1, 1, (t, k)).astype(np.float32)
+        dz = sm.gate_backward(r, gp)
+        logits = rng.standard_normal((t, e)).astype(np.float32)
+        sr = sm.softmax_rows(Matrix(logits))
+        r2 = sm.topk_select(sr, k, renormalize=renorm)
+        pre = f"g{j}_"
+        out.update({pre + "x": x.data, pre + "wg": wg.data, pre + "gate": gate.data, pre + "idx": r.expert_idx,
+                    pre + "p": r.p, pre + "k": np.int64(k), pre + "renorm": np.int64(renorm), pre + "grad_p": gp,
+                    pre + "dz": dz.data, pre + "logits": logits, pre + "soft": sr.data, pre + "idx2": r2.expert_idx,
+                    pre + "p2": r2.p})
+        j += 1
+    # ties: all-equal rows and duplicated maxima
+    tie = np.zeros((3, 6), dtype=np.float32)
+    tie[1, [2, 4]] = 1.0
+    tie[2, :] = [0.5, 0.1, 0.5, 0.1, 0.5, 0.0]
+    rt = sm.topk_select(Matrix(tie), 3, renormalize=False)
+    out.update({"tie_gate": tie, "tie_idx": rt.expert_idx, "num_gate": np.int64(j)})
+    np.savez_compressed(HERE / "gate.npz", **out)
+
+
 if __name__ == "__main__":
+    gate_fixtures()
     routing_fixtures()
     kernel_fixtures()
     mlp_fixtures()

@@ -116,3 +116,24 @@ def test_seeded_problem_matches_reference_draws():
     np.testing.assert_array_equal(idx, g["mlp5_idx"])
     np.testing.assert_array_equal(p, g["mlp5_p"])
     np.testing.assert_array_equal(dy, g["mlp5_dy"])
+
+
+def test_gate_topk_and_backward():
+    """gate_forward / topk_select / gate_backward against the reference's outputs."""
+    g = load_golden("gate")
+    for j in range(int(g["num_gate"])):
+        pre = f"g{j}_"
+        k, renorm = int(g[pre + "k"]), bool(g[pre + "renorm"])
+        gate = orc.gate_probs(g[pre + "x"], g[pre + "wg"])
+        np.testing.assert_array_equal(gate, g[pre + "gate"])
+        order = np.argsort(-gate, axis=1, kind="stable")[:, :k]
+        assert np.array_equal(order, g[pre + "idx"])
+        if renorm:
+            idx, p = orc.topk_routing(gate, k)
+            assert np.array_equal(idx, g[pre + "idx"])
+            np.testing.assert_allclose(p, g[pre + "p"], rtol=1e-6, atol=1e-7)
+        dz = orc.gate_backward(gate, g[pre + "idx"], g[pre + "grad_p"], renorm)
+        np.testing.assert_allclose(dz, g[pre + "dz"], rtol=1e-5, atol=1e-7)
+        np.testing.assert_allclose(orc.softmax_rows(g[pre + "logits"]), g[pre + "soft"], rtol=1e-6, atol=1e-8)
+    tie = g["tie_gate"]
+    assert np.array_equal(np.argsort(-tie, axis=1, kind="stable")[:, :3], g["tie_idx"])
