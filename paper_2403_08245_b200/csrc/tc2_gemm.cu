@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
               tma_load_2d_cg2(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
             }
             if (AM == A_ROWS) {
-              tma_load_2d_cg2(&tma_a, fb, sa, kk, m_half);
+              tma_load_2d_cg2(&tma_a, fb, sa, (int)(tl.k0 + kk), m_half);
             } else if (AM == A_MN) {
               tma_load_2d_cg2(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
               tma_load_2d_cg2(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
