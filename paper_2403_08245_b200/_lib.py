@@ -14,7 +14,9 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libsmoe_b200.so"
+# SMOE_LIB overrides the in-tree library (used by scripts/ab.sh to A/B two builds
+# of the same C ABI inside one GPU session).
+LIB_PATH = Path(os.environ["SMOE_LIB"]) if os.environ.get("SMOE_LIB") else _PKG / "libsmoe_b200.so"
 
 SMOE_OK, SMOE_EINVAL, SMOE_ESHAPE, SMOE_ECUDA, SMOE_ENOTSUP = range(5)
 SMOE_F32, SMOE_BF16 = 0, 1

@@ -29,7 +29,12 @@ namespace tc2 {
 
 using namespace smoe::tc;
 
-constexpr int TM = 256, TN = 256, BK = 64, STAGES = 7;
+constexpr int TM = 256, TN = 256, BK = 64;
+// Gather-mode kernels stage their epilogue through shared memory (their cp.async
+// operand traffic shares the LSU with the stores) and give up one ring stage for
+// it; the TMA-fed kernels keep 7 stages and store directly (measured better).
+__host__ __device__ constexpr bool staged_epilogue(int am) { return am == 1; }
+__host__ __device__ constexpr int ring_stages(int am) { return staged_epilogue(am) ? 6 : 7; }
 constexpr int HM = TM / 2, HN = TN / 2;  // per-CTA halves
 constexpr int A_BYTES = HM * BK * 2;     // 16 KB
 constexpr int B_BYTES = HN * BK * 2;     // 16 KB
@@ -45,6 +50,7 @@ constexpr int G_RSTEP = GATHER_WARPS * 4;   // rows covered by one pass of all g
 constexpr int TG_ROWS = 0;
 constexpr int G_RPT = (128 - TG_ROWS) / G_RSTEP;  // rows per cp.async gather thread per k-block
 constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
+constexpr int STG_BYTES = 32 * 128;        // per-epilogue-warp staging tile: 32 rows x 64 bf16
 __host__ __device__ constexpr int kernel_threads(int am) {
   return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
 }
@@ -53,6 +59,8 @@ template <int AM, int BMODE, bool GK>
 __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, Params p) {
   constexpr int THREADS = kernel_threads(AM);
+  constexpr int STAGES = ring_stages(AM);
+  constexpr bool STAGED = staged_epilogue(AM);
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
   // critical producer and MMA warps take the highest ids and never queue behind
   // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
@@ -63,7 +71,8 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
-  uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  uint8_t *staging = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][STG_BYTES]
+  uint64_t *bars = (uint64_t *)(staging + (STAGED ? EPI_WARPS * STG_BYTES : 0));
   uint64_t *lfull_bar = bars;                    // [STAGES]
   // relay payload (16 B) + landing slot (16 B), 16-byte aligned inside bars[STAGES, 2*STAGES)
   uint8_t *signal = (uint8_t *)((((uintptr_t)(bars + STAGES)) + 15) & ~(uintptr_t)15);
@@ -266,70 +275,158 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       }
     }
   } else if (warp < EPI_WARPS) {
-    // ===================== epilogue (own 128 rows) =====================
-    const int ew = warp;
-    const int q = warp & 3;
-    const int c_begin = (ew / 4) * EPI_COLS;
-    const int r = q * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int64_t t = cluster_id; t < total; t += num_clusters) {
-      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
-      const int64_t row = tl.m0 + HM * rank + r;
-      const bool valid = row < tl.m_end;
-      __nv_bfloat16 *orow = nullptr, *orow2 = nullptr;
-      const __nv_bfloat16 *arow = nullptr;
-      if (valid) {
-        int64_t dst;
-        if (GK) dst = (int64_t)tl.e * p.M + row;
-        else dst = p.grouped_out ? row : (int64_t)p.order[row];
-        orow = p.out + dst * p.N;
-        if (p.out2) orow2 = p.out2 + dst * p.N;
-        if (p.aux) arow = p.aux + dst * p.N;
-      }
-      const bool has_acc = tl.nkb > 0;
-      uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      const bool use_aux = (p.epi == SMOE_EPI_ACT_GRAD) && valid;
-      if (use_aux) {
-        const int64_t c0 = tl.n0 + c_begin;
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (c0 + 8 * j < p.N) av[j] = __ldg(reinterpret_cast<const uint4 *>(arow + c0 + 8 * j));
-      }
-      if (has_acc) {
-        mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
-        tc_fence_after();
-      }
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
-#pragma unroll 1
-      for (int c = 0; c < EPI_COLS; c += 16) {
-        uint32_t v[16];
+    if constexpr (STAGED) {
+      // ===================== epilogue (own 128 rows) =====================
+      // TMEM -> registers -> activation math -> a per-warp 4 KB staging tile ->
+      // coalesced global stores (8 lanes per 128-byte row segment, 4 rows per
+      // instruction).  Row-per-thread stores touch 32 lines per instruction and
+      // cost up to 16 % of the tensor pipe on C1 layer 1 (base-clock ncu); the
+      // act-grad operand (h_pre) is read through the same staging tile.
+      const int q = warp & 3;
+      const int c_begin = (warp / 4) * EPI_COLS;
+      const int r = q * 32 + lane;
+      const uint32_t stg = smem_u32(staging + warp * STG_BYTES);
+      const int cr = lane >> 3, cc = lane & 7;  // copy role: rows cr + 4 i, 16-byte chunk cc
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const int64_t row = tl.m0 + HM * rank + r;
+        long long dst = -1;
+        if (row < tl.m_end) dst = GK ? (int64_t)tl.e * p.M + row : (p.grouped_out ? row : (int64_t)p.order[row]);
+        long long cdst[8];
+  #pragma unroll
+        for (int i = 0; i < 8; ++i) cdst[i] = __shfl_sync(0xffffffffu, dst, cr + 4 * i);
+        const bool has_acc = tl.nkb > 0;
         if (has_acc) {
-          tmem_ld16(tbase + c, v);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0u;
+          mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
+          tc_fence_after();
         }
-        const int64_t col0 = tl.n0 + c_begin + c;
-        uint4 avn[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-        if (use_aux && c + 16 < EPI_COLS) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            if (col0 + 16 + 8 * j < p.N) avn[j] = __ldg(reinterpret_cast<const uint4 *>(arow + col0 + 16 + 8 * j));
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
+  #pragma unroll 1
+        for (int cg = 0; cg < EPI_COLS; cg += 64) {
+          const int64_t col0 = tl.n0 + c_begin + cg;
+          const bool col_ok = col0 + cc * 8 < p.N;
+          if (p.epi == SMOE_EPI_ACT_GRAD) {
+            // coalesced read of the 32 rows' h_pre segments into the staging tile
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int rl = cr + 4 * i;
+              uint4 val = make_uint4(0, 0, 0, 0);
+              if (cdst[i] >= 0 && col_ok) val = __ldg(reinterpret_cast<const uint4 *>(p.aux + cdst[i] * p.N + col0 + cc * 8));
+              sts128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4), val);
+            }
+            __syncwarp();
+          }
+          // one pass per output (EPI_ACT writes h_pre, then act(h_pre) from a TMEM re-read);
+          // each pass builds this lane's 128-byte row segment in two 32-column halves
+          const int passes = (p.epi == SMOE_EPI_ACT) ? 2 : 1;
+          for (int pass = 0; pass < passes; ++pass) {
+  #pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t v[32];
+              if (has_acc) {
+                tmem_ld16(tbase + cg + 32 * hf, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(tbase + cg + 32 * hf + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+              } else {
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0u;
+              }
+              uint32_t io[16];
+              if (p.epi == SMOE_EPI_ACT_GRAD) {
+  #pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const uint4 val = lds128(stg + lane * 128 + (((4 * hf + c) ^ (lane & 7)) << 4));
+                  io[4 * c] = val.x; io[4 * c + 1] = val.y; io[4 * c + 2] = val.z; io[4 * c + 3] = val.w;
+                }
+              }
+              if (has_acc) tmem_ld_wait();
+              epilogue_pack32(p, v, io, pass == 1);
+  #pragma unroll
+              for (int c = 0; c < 4; ++c)
+                sts128(stg + lane * 128 + (((4 * hf + c) ^ (lane & 7)) << 4),
+                       make_uint4(io[4 * c], io[4 * c + 1], io[4 * c + 2], io[4 * c + 3]));
+            }
+            __syncwarp();
+            store_staged_rows(stg, pass == 0 ? p.out : p.out2, cdst, col0, col_ok, p.N, cr, cc);
+          }
         }
-        if (has_acc) tmem_ld_wait();
-        if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0);
-        av[0] = avn[0];
-        av[1] = avn[1];
+        if (has_acc) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive(smem_u32(&tempty_bar[acc]));
+            else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+          }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
       }
-      if (has_acc) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(smem_u32(&tempty_bar[acc]));
-          else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+    } else {
+      // ---- direct epilogue: each thread stores its own row ----
+      const int ew = warp;
+      const int q = warp & 3;
+      const int c_begin = (ew / 4) * EPI_COLS;
+      const int r = q * 32 + lane;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const int64_t row = tl.m0 + HM * rank + r;
+        const bool valid = row < tl.m_end;
+        __nv_bfloat16 *orow = nullptr, *orow2 = nullptr;
+        const __nv_bfloat16 *arow = nullptr;
+        if (valid) {
+          int64_t dst;
+          if (GK) dst = (int64_t)tl.e * p.M + row;
+          else dst = p.grouped_out ? row : (int64_t)p.order[row];
+          orow = p.out + dst * p.N;
+          if (p.out2) orow2 = p.out2 + dst * p.N;
+          if (p.aux) arow = p.aux + dst * p.N;
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        const bool has_acc = tl.nkb > 0;
+        uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        const bool use_aux = (p.epi == SMOE_EPI_ACT_GRAD) && valid;
+        if (use_aux) {
+          const int64_t c0 = tl.n0 + c_begin;
+  #pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (c0 + 8 * j < p.N) av[j] = __ldg(reinterpret_cast<const uint4 *>(arow + c0 + 8 * j));
+        }
+        if (has_acc) {
+          mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
+          tc_fence_after();
+        }
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
+  #pragma unroll 1
+        for (int c = 0; c < EPI_COLS; c += 16) {
+          uint32_t v[16];
+          if (has_acc) {
+            tmem_ld16(tbase + c, v);
+          } else {
+  #pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0u;
+          }
+          const int64_t col0 = tl.n0 + c_begin + c;
+          uint4 avn[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+          if (use_aux && c + 16 < EPI_COLS) {
+  #pragma unroll
+            for (int j = 0; j < 2; ++j)
+              if (col0 + 16 + 8 * j < p.N) avn[j] = __ldg(reinterpret_cast<const uint4 *>(arow + col0 + 16 + 8 * j));
+          }
+          if (has_acc) tmem_ld_wait();
+          if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0);
+          av[0] = avn[0];
+          av[1] = avn[1];
+        }
+        if (has_acc) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive(smem_u32(&tempty_bar[acc]));
+            else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+          }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
       }
     }
   } else if (AM == A_GATHER) {
@@ -396,12 +493,24 @@ static int group_m_k_setting() {
   return gm;
 }
 
-static size_t smem_bytes(int E) { return 1024 + STAGES * STAGE_BYTES + 8 * (3 * STAGES + 6) + 12 * (E + 1) + 64; }
+static size_t smem_bytes(int E, int am) {
+  const int stages = ring_stages(am);
+  return 1024 + stages * STAGE_BYTES + (staged_epilogue(am) ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 6) +
+         12 * (E + 1) + 64;
+}
+
+}  // namespace tc2
+
+bool tc2_supports_experts(int E) {
+  return tc2::smem_bytes(E, tc::A_GATHER) <= 232448 && tc2::smem_bytes(E, tc::A_ROWS) <= 232448;
+}
+
+namespace tc2 {
 
 template <int AM, int BMODE, bool GK>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, int64_t max_tiles, cudaStream_t st) {
   auto kern = tc2_gemm_kernel<AM, BMODE, GK>;
-  size_t smem = smem_bytes(p.E);
+  size_t smem = smem_bytes(p.E, AM);
   static size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

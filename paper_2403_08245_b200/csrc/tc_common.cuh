@@ -355,5 +355,59 @@ __device__ __forceinline__ void bulk_signal_cta0(uint32_t dst_local, uint32_t sr
                "r"(src_local), "r"(bar)
                : "memory");
 }
+
+// ---- staged epilogue helpers (CTA-pair kernel) -----------------------------------
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// 32 fp32 accumulators of one row -> 16 packed bf16x2 words in io.
+//   act_pass = false: round(acc) (EPI_NONE / EPI_ACT's pre-activation) or, for
+//                     EPI_ACT_ONLY, act(round(acc)); for EPI_ACT_GRAD io holds the
+//                     32 bf16 of h_pre on entry and acc * act'(h_pre) on return;
+//   act_pass = true : act(round(acc)) (EPI_ACT's second output).
+__device__ __forceinline__ void epilogue_pack32(const Params &p, const uint32_t (&v)[32], uint32_t (&io)[16],
+                                                bool act_pass) {
+  const bool apply_act = act_pass || p.epi == SMOE_EPI_ACT_ONLY;
+  if (p.epi == SMOE_EPI_ACT_GRAD) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&io[i]);
+      io[i] = pack_bf16(__uint_as_float(v[2 * i]) * act_grad_fast(p.act, __bfloat162float(a.x)),
+                        __uint_as_float(v[2 * i + 1]) * act_grad_fast(p.act, __bfloat162float(a.y)));
+    }
+  } else if (apply_act) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const __nv_bfloat162 pre = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+      io[i] = pack_bf16(act_fwd_fast(p.act, __bfloat162float(pre.x)), act_fwd_fast(p.act, __bfloat162float(pre.y)));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) io[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+  }
+}
+
+// Coalesced copy of a warp's staging tile (32 rows x 128 B, 16-byte chunks
+// XOR-swizzled by row) to global: lane (cr, cc) writes chunk cc of rows
+// cr + 4 i to row cdst[i] (< 0: masked) of `base` — 4 full 128-byte row
+// segments per store instruction instead of 32 scattered 16-byte pieces.
+__device__ __forceinline__ void store_staged_rows(uint32_t stg, __nv_bfloat16 *base, const long long (&cdst)[8],
+                                                  int64_t col0, bool col_ok, int64_t ld, int cr, int cc) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rl = cr + 4 * i;
+    const uint4 val = lds128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4));
+    if (cdst[i] >= 0 && col_ok) *reinterpret_cast<uint4 *>(base + cdst[i] * ld + col0 + cc * 8) = val;
+  }
+  __syncwarp();
+}
 }  // namespace tc
 }  // namespace smoe

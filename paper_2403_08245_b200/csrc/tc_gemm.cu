@@ -398,6 +398,7 @@ int scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, 
                     int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
 }  // namespace tc2
+bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
 // 2 = CTA-pair kernels (tc2_gemm.cu, default), 1 = single-CTA kernels (this file).
 static int tc_ctas() {
@@ -423,7 +424,7 @@ int tc_scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int6
   if (!tc_supports_s2s(d_in, d_out, x, w, out))
     return fail(SMOE_ENOTSUP, "tcgen05 scatter2scatter needs d_in, d_out multiples of 8 and 16-byte aligned buffers");
   if (E > 1024) return fail(SMOE_ENOTSUP, "tcgen05 path supports up to 1024 experts");
-  if (tc_ctas() == 2)
+  if (tc_ctas() == 2 && tc2_supports_experts(E))
     return tc2::scatter2scatter(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi,
                                 act, out, out2, aux, st);
   CUtensorMap ta, tb;
@@ -474,7 +475,7 @@ int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, 
   if (!(d_in % 8 == 0 && d_out % 8 == 0 && al16(xg) && al16(yg) && al16(dw)))
     return fail(SMOE_ENOTSUP, "tcgen05 group_xty needs d_in, d_out multiples of 8 and 16-byte aligned buffers");
   if (E > 1024) return fail(SMOE_ENOTSUP, "tcgen05 path supports up to 1024 experts");
-  if (tc_ctas() == 2) return tc2::group_xty(xg, yg, offsets, E, n, d_in, d_out, dw, st);
+  if (tc_ctas() == 2 && tc2_supports_experts(E)) return tc2::group_xty(xg, yg, offsets, E, n, d_in, d_out, dw, st);
   CUtensorMap ta, tb;
   uint64_t rows = (uint64_t)(n > 0 ? n : 1);
   {

@@ -1,0 +1,21 @@
+#!/bin/bash
+# Build libsmoe_b200.so from a git revision into scripts/_bin/libsmoe_<name>.so
+# (A/B comparisons inside one GPU session: SMOE_LIB=scripts/_bin/libsmoe_<name>.so).
+# usage: build_variant.sh REV NAME
+set -e
+rev=$1; name=$2
+root=$(cd "$(dirname "$0")/.." && pwd)
+tmp=$(mktemp -d)
+git -C "$root" archive "$rev" paper_2403_08245_b200/csrc include | tar -x -C "$tmp"
+objs=()
+for f in "$tmp"/paper_2403_08245_b200/csrc/*.cu; do
+  o="$tmp/$(basename "$f" .cu).o"
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
+    -I "$tmp/include" -c "$f" -o "$o" &
+  objs+=("$o")
+done
+wait
+mkdir -p "$root/scripts/_bin"
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC "${objs[@]}" -o "$root/scripts/_bin/libsmoe_$name.so"
+rm -rf "$tmp"
+echo "$root/scripts/_bin/libsmoe_$name.so"
