@@ -30,11 +30,14 @@ namespace tc2 {
 using namespace smoe::tc;
 
 constexpr int TM = 256, TN = 256, BK = 64;
-// Gather-mode kernels stage their epilogue through shared memory (their cp.async
-// operand traffic shares the LSU with the stores) and give up one ring stage for
-// it; the TMA-fed kernels keep 7 stages and store directly (measured better).
-__host__ __device__ constexpr bool staged_epilogue(int am) { return am == 1; }
-__host__ __device__ constexpr int ring_stages(int am) { return staged_epilogue(am) ? 6 : 7; }
+// Epilogue styles (template STAGED):
+//   direct : each thread stores its own accumulator row (7-stage ring);
+//   staged : rows go through a per-warp 4 KB smem tile (6-stage ring) and leave
+//            as one TMA tile store (grouped outputs, full 32-row slabs) or as
+//            coalesced 128-byte row segments (scattered outputs, bin tails).
+// Gather-mode kernels always stage (their cp.async operand traffic shares the
+// LSU with the stores); which TMA-fed kernels stage is chosen per launch.
+__host__ __device__ constexpr int ring_stages(bool staged) { return staged ? 6 : 7; }
 constexpr int HM = TM / 2, HN = TN / 2;  // per-CTA halves
 constexpr int A_BYTES = HM * BK * 2;     // 16 KB
 constexpr int B_BYTES = HN * BK * 2;     // 16 KB
@@ -55,12 +58,12 @@ __host__ __device__ constexpr int kernel_threads(int am) {
   return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
 }
 
-template <int AM, int BMODE, bool GK>
+template <int AM, int BMODE, bool GK, bool STAGED>
 __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 1)
-    tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, Params p) {
+    tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                    const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_c2, Params p) {
   constexpr int THREADS = kernel_threads(AM);
-  constexpr int STAGES = ring_stages(AM);
-  constexpr bool STAGED = staged_epilogue(AM);
+  constexpr int STAGES = ring_stages(STAGED);
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
   // critical producer and MMA warps take the highest ids and never queue behind
   // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
@@ -287,11 +290,17 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       const int r = q * 32 + lane;
       const uint32_t stg = smem_u32(staging + warp * STG_BYTES);
       const int cr = lane >> 3, cc = lane & 7;  // copy role: rows cr + 4 i, 16-byte chunk cc
+      // grouped outputs are contiguous row ranges: whole 32-row slabs leave by TMA
+      const bool tma_out = GK || p.grouped_out;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t t = cluster_id; t < total; t += num_clusters) {
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         const int64_t row = tl.m0 + HM * rank + r;
+        const int64_t slab0 = tl.m0 + HM * rank + q * 32;
+        // a slab straddling the bin end must not touch the next expert's rows
+        const bool slab_tma = tma_out && slab0 + 32 <= tl.m_end;
+        const int slab_row = (int)(GK ? (int64_t)tl.e * p.M + slab0 : slab0);
         long long dst = -1;
         if (row < tl.m_end) dst = GK ? (int64_t)tl.e * p.M + row : (p.grouped_out ? row : (int64_t)p.order[row]);
         long long cdst[8];
@@ -307,6 +316,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         for (int cg = 0; cg < EPI_COLS; cg += 64) {
           const int64_t col0 = tl.n0 + c_begin + cg;
           const bool col_ok = col0 + cc * 8 < p.N;
+          if (col0 >= p.N) break;
+          // the staging tile is reused: the previous TMA store must have read it
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
           if (p.epi == SMOE_EPI_ACT_GRAD) {
             // coalesced read of the 32 rows' h_pre segments into the staging tile
   #pragma unroll
@@ -347,8 +360,19 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
                 sts128(stg + lane * 128 + (((4 * hf + c) ^ (lane & 7)) << 4),
                        make_uint4(io[4 * c], io[4 * c + 1], io[4 * c + 2], io[4 * c + 3]));
             }
-            __syncwarp();
-            store_staged_rows(stg, pass == 0 ? p.out : p.out2, cdst, col0, col_ok, p.N, cr, cc);
+            if (slab_tma) {
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(pass == 0 ? &tma_c : &tma_c2, stg, (int)col0, slab_row);
+                bulk_commit();
+                if (pass + 1 < passes) bulk_wait_read0();
+              }
+              __syncwarp();
+            } else {
+              __syncwarp();
+              store_staged_rows(stg, pass == 0 ? p.out : p.out2, cdst, col0, col_ok, p.N, cr, cc);
+            }
           }
         }
         if (has_acc) {
@@ -361,6 +385,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
+      if (lane == 0) bulk_wait0();
     } else {
       // ---- direct epilogue: each thread stores its own row ----
       const int ew = warp;
@@ -493,24 +518,24 @@ static int group_m_k_setting() {
   return gm;
 }
 
-static size_t smem_bytes(int E, int am) {
-  const int stages = ring_stages(am);
-  return 1024 + stages * STAGE_BYTES + (staged_epilogue(am) ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 6) +
-         12 * (E + 1) + 64;
+static size_t smem_bytes(int E, bool staged) {
+  const int stages = ring_stages(staged);
+  return 1024 + stages * STAGE_BYTES + (staged ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 6) + 12 * (E + 1) + 64;
 }
 
 }  // namespace tc2
 
 bool tc2_supports_experts(int E) {
-  return tc2::smem_bytes(E, tc::A_GATHER) <= 232448 && tc2::smem_bytes(E, tc::A_ROWS) <= 232448;
+  return tc2::smem_bytes(E, true) <= 232448 && tc2::smem_bytes(E, false) <= 232448;
 }
 
 namespace tc2 {
 
-template <int AM, int BMODE, bool GK>
-static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, int64_t max_tiles, cudaStream_t st) {
-  auto kern = tc2_gemm_kernel<AM, BMODE, GK>;
-  size_t smem = smem_bytes(p.E, AM);
+template <int AM, int BMODE, bool GK, bool STAGED>
+static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &tc, const CUtensorMap &tc2,
+                  const Params &p, int64_t max_tiles, cudaStream_t st) {
+  auto kern = tc2_gemm_kernel<AM, BMODE, GK, STAGED>;
+  size_t smem = smem_bytes(p.E, STAGED);
   static size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -519,8 +544,30 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p,
   }
   int clusters = num_sms() / 2;
   if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
-  tc2_gemm_kernel<AM, BMODE, GK><<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, p);
+  kern<<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, tc, tc2, p);
   return check_launch("tc2_gemm");
+}
+
+// Which kernels stage their epilogue (see ring_stages): the gather-mode kernels.
+// For the TMA-fed kernels the 7th ring stage is worth more than TMA stores
+// (base-clock ncu, C1: rows 88.2 -> 86.8 %, dh 81.0 -> 79.7 %, xty 70.1 -> 69.3 %
+// tensor-pipe active when staged; gather 75.0 -> 77.0 %, l1 68.4 -> 70.6 %).
+// SMOE_TC_EPI=all stages every grouped-output kernel too (A/B experiments).
+static bool staged_for(bool gather, bool grouped_out) {
+  static int all = -1;
+  if (all < 0) {
+    const char *env = getenv("SMOE_TC_EPI");
+    all = (env && !strcmp(env, "all")) ? 1 : 0;
+  }
+  return gather || (all && grouped_out);
+}
+
+// Output tile map for TMA stores: [rows, cols] bf16, 32-row x 64-column boxes.
+static bool encode_out_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols) {
+  uint64_t dims[2] = {(uint64_t)cols, (uint64_t)(rows > 0 ? rows : 1)};
+  uint64_t strides[1] = {(uint64_t)cols * 2};
+  uint32_t box[2] = {64, 32};
+  return encode_map(m, ptr, 2, dims, strides, box);
 }
 
 int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
@@ -559,12 +606,21 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.group_m = (group_m_setting() + 1) / 2;
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
-  if (gin) {
-    if (!trans) return launch<A_ROWS, B_W_MN, false>(ta, tb, p, max_tiles, st);
-    return launch<A_ROWS, B_W_K, false>(ta, tb, p, max_tiles, st);
+  CUtensorMap tc = ta, tc2 = ta;  // unused unless the output is grouped
+  if (gout) {
+    if (!encode_out_map(&tc, out, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out) failed");
+    if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
-  if (!trans) return launch<A_GATHER, B_W_MN, false>(ta, tb, p, max_tiles, st);
-  return launch<A_GATHER, B_W_K, false>(ta, tb, p, max_tiles, st);
+  if (gin) {
+    if (staged_for(false, gout)) {
+      if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
+      return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
+    }
+    if (!trans) return launch<A_ROWS, B_W_MN, false, false>(ta, tb, tc, tc2, p, max_tiles, st);
+    return launch<A_ROWS, B_W_K, false, false>(ta, tb, tc, tc2, p, max_tiles, st);
+  }
+  if (!trans) return launch<A_GATHER, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
+  return launch<A_GATHER, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
 }
 
 int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in, int64_t d_out,
@@ -596,7 +652,10 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   p.group_m = group_m_k_setting();
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
-  return launch<A_MN, B_ROWS_MN, true>(ta, tb, p, max_tiles, st);
+  CUtensorMap tc;
+  if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
+  if (staged_for(false, true)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);
+  return launch<A_MN, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
 }
 
 }  // namespace tc2

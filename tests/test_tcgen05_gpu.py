@@ -96,3 +96,35 @@ torch.save((y.cpu(), dw.cpu()), sys.argv[1])
     (y2, dw2), (y1, dw1) = outs
     assert torch.equal(y1, y2)          # same products, same fp32 accumulation order per K block
     assert _rel(dw1, dw2) < 1e-3
+
+
+def test_tma_store_epilogue_matches_direct():
+    """SMOE_TC_EPI=all (staged TMA-store epilogue on every grouped-output kernel)
+    is bit-identical to the default direct-store epilogue: bin tails, column
+    tails, fused activation / activation-grad outputs and group_xty."""
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2403_08245_b200 as sm
+torch.manual_seed(1)
+t, k, e, d, de = 1900, 2, 8, 264, 584
+ids = torch.stack([torch.randperm(e)[:k] for _ in range(t)]).cuda()
+r = sm.RoutingResult(ids, torch.rand(t, k, device='cuda'), torch.zeros(t, e, device='cuda'), renormalized=False, validate=False)
+o = sm.compute_grouped_order(r)
+x = (torch.rand(t * k, d, device='cuda') * 2 - 1).bfloat16()
+w = ((torch.rand(e, d, de, device='cuda') * 2 - 1) / 16).bfloat16()
+h = torch.empty(t * k, de, device='cuda', dtype=torch.bfloat16)
+a = torch.empty_like(h)
+sm.scatter2scatter(x, w, o, 1, sm.GROUPED_TO_GROUPED, out=h, activation='gelu', act_out=a, engine='tcgen05')
+g = sm.scatter2scatter(x, w, o, 1, sm.GROUPED_TO_GROUPED, activation='gelu', act_grad_of=h, engine='tcgen05')
+dw = sm.group_xty(x, h, o, engine='tcgen05')
+torch.save((h.cpu(), a.cpu(), g.cpu(), dw.cpu()), sys.argv[1])
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("default", "all"):
+        path = f"/tmp/smoe_epi_{mode}.pt"
+        env = dict(os.environ, SMOE_TC_EPI=mode)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300)
+        outs.append(torch.load(path))
+    for u, v in zip(*outs):
+        assert torch.equal(u, v)
