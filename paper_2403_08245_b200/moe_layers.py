@@ -15,7 +15,9 @@ B200 changes (same results, fewer passes over HBM):
 The buffer-reuse discipline of smoe_mlp_backward (:198-211) is kept exactly.
 
 The attention core of MoMHA (between the two routed projections) is outside
-the ParallelLinear hot path; it runs as plain torch GPU ops.
+the ParallelLinear hot path: it runs as torch's fused
+scaled-dot-product attention (library flash / cuDNN kernels) in grouped-query
+form, and the shared K/V projections as library GEMMs.
 """
 from __future__ import annotations
 
@@ -280,22 +282,27 @@ def _attn_core(q, keys, values, seq_len, d_head, k, causal):
     """Slot queries (T*k, d_proj) in chronological order vs dense K/V (T, d_proj).
 
     Query head (slot, j) attends with K/V head j of its sequence; causal within
-    the sequence (moe_layers.py:280-327).  float32 math.
+    the sequence (moe_layers.py:280-327).  The k slots of a token sit at the
+    token's position, so the core is causal attention with k query heads per
+    K/V head (grouped-query layout): query head hh*k + j of a token is its slot
+    j's head hh.  Runs as one fused scaled-dot-product attention (flash /
+    cuDNN kernels for bf16), in the input dtype.
     """
     n = keys.shape[0]
     b = n // seq_len
     h = q.shape[1] // d_head
-    qf = q.float().view(b, seq_len * k, h, d_head).transpose(1, 2)          # (b, h, L*k, dh)
-    kf = keys.float().view(b, seq_len, h, d_head).transpose(1, 2)           # (b, h, L, dh)
-    vf = values.float().view(b, seq_len, h, d_head).transpose(1, 2)
-    scores = (qf @ kf.transpose(-1, -2)) * (1.0 / math.sqrt(d_head))        # (b, h, L*k, L)
-    if causal:
-        qt = torch.arange(seq_len * k, device=q.device) // k
-        kt = torch.arange(seq_len, device=q.device)
-        scores = scores.masked_fill(qt[:, None] < kt[None, :], float("-inf"))
-    probs = torch.softmax(scores, dim=-1)
-    out = probs @ vf                                                         # (b, h, L*k, dh)
-    return out.transpose(1, 2).reshape(b * seq_len * k, h * d_head)
+    qh = q.view(b, seq_len, k, h, d_head).permute(0, 3, 2, 1, 4).reshape(b, h * k, seq_len, d_head)
+    kh = keys.view(b, seq_len, h, d_head).transpose(1, 2).repeat_interleave(k, dim=1)
+    vh = values.view(b, seq_len, h, d_head).transpose(1, 2).repeat_interleave(k, dim=1)
+    out = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=causal)
+    return out.view(b, h, k, seq_len, d_head).permute(0, 3, 2, 1, 4).reshape(b * seq_len * k, h * d_head)
+
+
+def _mm(a, b):
+    """Dense projection: bf16 on the tensor cores with fp32 accumulation, fp32 exact-mode in fp32."""
+    if a.dtype == torch.float32:
+        return a @ b
+    return (a @ b).to(a.dtype)
 
 
 def attention(q, keys, values, slot_tokens, seq_len, d_head, causal=True):
@@ -311,7 +318,7 @@ def attention(q, keys, values, slot_tokens, seq_len, d_head, causal=True):
     if n % seq_len:
         raise ValueError(f"token count {n} is not divisible by seq_len {seq_len}")
     k = q.shape[0] // n
-    return _attn_core(q, keys, values, seq_len, d_head, k, causal).to(q.dtype)
+    return _attn_core(q, keys, values, seq_len, d_head, k, causal)
 
 
 def attention_backward(q, keys, values, slot_tokens, seq_len, d_head, causal, d_out):
@@ -319,12 +326,12 @@ def attention_backward(q, keys, values, slot_tokens, seq_len, d_head, causal, d_
     n = keys.shape[0]
     k = q.shape[0] // n
     with torch.enable_grad():
-        qv = q.detach().float().requires_grad_(True)
-        kv = keys.detach().float().requires_grad_(True)
-        vv = values.detach().float().requires_grad_(True)
+        qv = q.detach().requires_grad_(True)
+        kv = keys.detach().requires_grad_(True)
+        vv = values.detach().requires_grad_(True)
         out = _attn_core(qv, kv, vv, seq_len, d_head, k, causal)
-        dq, dk, dv = torch.autograd.grad(out, (qv, kv, vv), d_out.float())
-    return dq.to(q.dtype), dk.to(q.dtype), dv.to(q.dtype)
+        dq, dk, dv = torch.autograd.grad(out, (qv, kv, vv), d_out.to(q.dtype))
+    return dq, dk, dv
 
 
 @dataclass
@@ -368,8 +375,8 @@ def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: Group
     if routing.num_tokens != n or routing.k != config.k:
         raise ValueError(f"routing covers {routing.num_tokens} tokens with k={routing.k}; "
                          f"expected {n} tokens with k={config.k}")
-    keys = (x.float() @ weights.wk.float()).to(x.dtype)
-    values = (x.float() @ weights.wv.float()).to(x.dtype)
+    keys = _mm(x, weights.wk)
+    values = _mm(x, weights.wv)
     q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=SCATTERED_TO_SCATTERED,
                               tile=tile, training=training, ledger=ledger, name="momha.query")
     attn_out = attention(q, keys, values, None, seq_len, config.d_head, config.causal)
@@ -389,9 +396,10 @@ def momha_backward(ctx: MomhaContext, dy, *, tile: TileConfig | None = None, led
     dq, dk, dv = attention_backward(ctx.q, ctx.keys, ctx.values, None, ctx.seq_len, ctx.d_head, ctx.causal,
                                     g_o.dx)
     g_q = pl.backward(ctx.query_ctx, dq, tile=tile, ledger=ledger, name="momha.query")
-    x32 = ctx.x.float()
-    dwk = (x32.t() @ dk.float()).to(ctx.x.dtype)
-    dwv = (x32.t() @ dv.float()).to(ctx.x.dtype)
-    dx_kv = dk.float() @ ctx.wk.float().t() + dv.float() @ ctx.wv.float().t()
-    dx = (g_q.dx.float() + dx_kv).to(ctx.x.dtype)
+    x = ctx.x
+    dwk = _mm(x.t(), dk)
+    dwv = _mm(x.t(), dv)
+    # dx = dx_q + dk Wk^T + dv Wv^T as one GEMM over the concatenated K/V gradients
+    dx_kv = torch.cat([dk, dv], 1) @ torch.cat([ctx.wk, ctx.wv], 1).t()
+    dx = (g_q.dx.float() + dx_kv.float()).to(x.dtype)
     return MomhaGradients(dx=dx, dwq=g_q.dw, dwk=dwk, dwv=dwv, dwo=g_o.dw, dp=g_o.dp)

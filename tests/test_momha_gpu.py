@@ -36,3 +36,23 @@ def test_momha_projection_shapes_c3_bf16():
     gr = sm.momha_backward(ctx, torch.ones_like(y))
     assert y.shape == (b * seq, 2048) and torch.isfinite(y.float()).all()
     assert torch.isfinite(gr.dwq.float()).all() and torch.isfinite(gr.dwo.float()).all()
+
+
+def test_momha_bf16_matches_fp32_path():
+    """bf16 MoMHA (tcgen05 projections + fused SDPA core) vs the fp32 path on the
+    same bf16-rounded inputs: rel. err <= 2e-2 per output and gradient."""
+    cfg = sm.MomhaConfig(d_model=256, d_head=64, num_heads=8, heads_per_expert=2, num_experts=8, k=4)
+    seq, b = 256, 3
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.rand((b * seq, 256), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand((b * seq, 256), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w16 = sm.init_momha_weights(cfg, 3, dtype=torch.bfloat16)
+    w32 = sm.MomhaWeights(*(getattr(w16, f).float() for f in ("wq", "wk", "wv", "wo")))
+    routing = sm.topk_select(torch.softmax(torch.randn(b * seq, 8, device="cuda", generator=g), 1), 4)
+    order = sm.compute_grouped_order(routing)
+    y16, c16 = sm.momha_forward(x, w16, routing, order, cfg, seq)
+    y32, c32 = sm.momha_forward(x.float(), w32, routing, order, cfg, seq)
+    assert rel_err(y16, y32.cpu().numpy()) <= 2e-2
+    g16, g32 = sm.momha_backward(c16, dy), sm.momha_backward(c32, dy.float())
+    for name in ("dx", "dwq", "dwk", "dwv", "dwo", "dp"):
+        assert rel_err(getattr(g16, name), getattr(g32, name).cpu().numpy()) <= 2e-2, name

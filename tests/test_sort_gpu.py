@@ -43,7 +43,8 @@ def test_reference_property_cases():
 
 
 @pytest.mark.parametrize("t,k,e", [(4096, 2, 8), (32768, 2, 8), (32768, 8, 64), (32768, 4, 16),
-                                   (5000, 3, 7), (1, 1, 1), (4097, 1, 1), (70000, 2, 1024)])
+                                   (5000, 3, 7), (1, 1, 1), (4097, 1, 1), (70000, 2, 1024),
+                                   (300001, 4, 1024), (600000, 2, 5), (262145, 4, 2)])
 def test_baseline_sizes_random(t, k, e):
     rng = np.random.default_rng(t + k + e)
     idx = np.stack([rng.permutation(e)[:k] for _ in range(min(t, 2000))])
