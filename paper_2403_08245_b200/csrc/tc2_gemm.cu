@@ -165,6 +165,15 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
             } else {
               tma_load_3d(&tma_b, fb, sb, kk, n_half, tl.e);
             }
+          } else if (GK && AM == A_MN && tl.k_len - kk < BK) {
+            // bin-tail stage of a grouped-K tile: each CTA counts its own bytes
+            // locally, zeroes its rows past the bin, and the peer then signals
+            // the leader (see the tail fixer below)
+            mbar_expect_tx(fb, STAGE_BYTES + (leader ? 16 : 0));
+            tma_load_2d(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
+            tma_load_2d(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
+            tma_load_2d(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
+            tma_load_2d(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
           } else {
             // both CTAs' bytes are counted on the leader's barrier
             if (leader) mbar_expect_tx(fb, 2 * STAGE_BYTES);
@@ -224,22 +233,25 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
           if (p.timing) c_lfull += clock64() - c1;
           uint8_t *sa_ptr = tiles_smem + stage * STAGE_BYTES;
+          int nk = BK / 16;  // K16 steps issued for this stage
           if (GK && kb == tl.nkb - 1) {
-            // bin tail: rows past the expert's bin belong to the next expert;
-            // zero them in both CTAs' tiles (peer via DSMEM) before the MMA.
+            // bin tail: rows past the expert's bin belong to the next expert.
+            // K16 steps wholly past the bin are skipped; the rest of the last
+            // partial step is zeroed by each CTA in its own tiles.
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             if (valid < BK) {
-              zero_k_tail(sa_ptr, 4, valid, lane);
-              zero_k_tail_peer(smem_u32(sa_ptr), 1, 4, valid, lane);
+              nk = (valid + 15) / 16;
+              if (valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
             }
           }
           if (RELAY) fence_proxy_async_smem();
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sa = smem_u32(sa_ptr);
-            const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa = smem_u32(sa_ptr);
+          const uint32_t sb = sa + A_BYTES;
+          if (elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
+              if (GK && k >= nk) break;
               uint64_t ad, bd;
               if (AM == A_MN) ad = sdesc(sa + k * 2048, 8192, 1024);
               else ad = sdesc(sa + k * 32, 16, 1024);
@@ -259,6 +271,30 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         printf("tc2 timing cluster %d: total %lld cyc, wait tempty %lld (%.1f%%), wait lfull %lld (%.1f%%)\n",
                (int)cluster_id, clock64() - c_start, c_tempty, 100.0 * c_tempty / (clock64() - c_start), c_lfull,
                100.0 * c_lfull / (clock64() - c_start));
+    } else if (GK) {
+      // ===================== tail fixer (peer CTA, grouped-K) =====================
+      // For each tile's bin-tail stage: wait for this CTA's own bytes, zero the
+      // A rows past the bin, then signal the leader's lfull (16-byte DSMEM bulk
+      // copy).  Non-tail stages never touch this CTA's lfull, so each stage's
+      // parity is tracked separately.
+      int stage = 0;
+      uint32_t parity_bits = 0;
+      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+          if (valid < BK) {
+            mbar_wait(smem_u32(&lfull_bar[stage]), (parity_bits >> stage) & 1u);
+            parity_bits ^= 1u << stage;
+            const int upto = 16 * ((valid + 15) / 16);  // the leader skips K16 steps past the bin
+            if (valid < upto) zero_k_rows(tiles_smem + stage * STAGE_BYTES, 4, valid, upto, lane);
+            else fence_proxy_async_smem();
+            if (lane == 0) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
+            __syncwarp();
+          }
+          if (++stage == STAGES) stage = 0;
+        }
+      }
     } else if (RELAY) {
       // ===================== relay (peer CTA, gather mode): own stage landed -> leader =====================
       int stage = 0;

@@ -143,6 +143,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// One lane of the (converged) warp; lets uniform values stay in uniform registers
+// around single-thread tcgen05 issue (no per-lane waterfall of R2UR moves).
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- cluster helpers (2-CTA pairs) ---------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -243,20 +253,23 @@ __device__ __forceinline__ Tile decode_tile(int64_t t, const Params &p, const in
   return tl;
 }
 
-// Zero K rows [valid, 64) of `boxes` consecutive 64-row x 128-B boxes (MN-major
+// Zero K rows [r0, r1) of `boxes` consecutive 64-row x 128-B boxes (MN-major
 // tiles); 128-B rows are swizzle-invariant as a whole.  Called by one warp.
-__device__ __forceinline__ void zero_k_tail(uint8_t *base, int boxes, int valid, int lane) {
-  const int rows = 64 - valid;
+__device__ __forceinline__ void zero_k_rows(uint8_t *base, int boxes, int r0, int r1, int lane) {
+  const int rows = r1 - r0;
   const int chunks = rows * boxes * 8;
   for (int c = lane; c < chunks; c += 32) {
     const int box = c / (rows * 8);
     const int rem = c - box * rows * 8;
-    const int r = valid + rem / 8;
+    const int r = r0 + rem / 8;
     const int q = rem % 8;
     *reinterpret_cast<uint4 *>(base + box * 8192 + r * 128 + q * 16) = make_uint4(0, 0, 0, 0);
   }
   fence_proxy_async_smem();
   __syncwarp();
+}
+__device__ __forceinline__ void zero_k_tail(uint8_t *base, int boxes, int valid, int lane) {
+  zero_k_rows(base, boxes, valid, 64, lane);
 }
 
 // Epilogue for one 16-column chunk of one accumulator row (fp32 in v[]).

@@ -17,7 +17,13 @@ xg = (torch.rand(n, d, device=dev, generator=g) * 2 - 1).bfloat16()
 w = ((torch.rand(E, d, de, device=dev, generator=g) * 2 - 1) / d ** 0.5).bfloat16()
 routing = sm.topk_select(torch.softmax(torch.randn(T, E, device=dev, generator=g), 1), k)
 order = sm.compute_grouped_order(routing)
-h = torch.empty(n, de, device=dev, dtype=torch.bfloat16)
+# operands with realistic values (uninitialised memory can hold NaN/Inf/denormal
+# patterns that change the tensor pipe's behaviour); SMOE_PROF_EMPTY=1 keeps the old behaviour
+import os  # noqa: E402
+if os.environ.get("SMOE_PROF_EMPTY"):
+    h = torch.empty(n, de, device=dev, dtype=torch.bfloat16)
+else:
+    h = ((torch.rand(n, de, device=dev, generator=g) * 2 - 1) * 0.5).bfloat16()
 h2 = torch.empty_like(h)
 for _ in range(3):
     if which == "l1":
@@ -38,6 +44,12 @@ for _ in range(3):
         sm.group_xty(xg, h, order)
     elif which == "xty":
         sm.group_xty(h, xg, order)
+    elif which == "xtyal":  # bins that are multiples of 64 (no K tails)
+        if _ == 0:
+            ids_al = (torch.arange(n, device=dev) % E).view(T, k)
+            r_al = sm.RoutingResult(ids_al, routing.p, routing.gate_full, renormalized=True, validate=False)
+            order_al = sm.compute_grouped_order(r_al)
+        sm.group_xty(h, xg, order_al)
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()
