@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         const uint32_t fb = smem_u32(&lfull_bar[stage]);
         const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
         const int kk = kb * BK;
-        if (lane == 0) {
-          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        // all lanes wait (keeps the warp converged, so coordinates and
+        // addresses stay in uniform registers); one elected lane issues
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        if (elect_one_sync()) {
           const uint32_t sb = sa + A_BYTES;
           if (RELAY) {
             // gather mode: this CTA's bytes are counted locally; the leader also
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
             const int upto = 16 * ((valid + 15) / 16);  // the leader skips K16 steps past the bin
             if (valid < upto) zero_k_rows(tiles_smem + stage * STAGE_BYTES, 4, valid, upto, lane);
             else fence_proxy_async_smem();
-            if (lane == 0) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
+            if (elect_one_sync()) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
             __syncwarp();
           }
           if (++stage == STAGES) stage = 0;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           // Signal the leader through the async proxy: a 16-byte DSMEM bulk copy
           // whose complete_tx lands on the leader's lfull[stage].  Unlike a
           // remote mbarrier.arrive it does not stall this thread.
-          if (lane == 0) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
+          if (elect_one_sync()) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
