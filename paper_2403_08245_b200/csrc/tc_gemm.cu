@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
 
   if (warp == WP) {
     // ===================== TMA producer (B, and A unless gathered) =====================
-    if (lane == 0) {
+    // The whole warp runs the schedule (converged: uniform operands); one
+    // elected lane issues.
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -127,25 +129,28 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
         for (int kb = 0; kb < tl.nkb; ++kb) {
           const uint32_t fb = smem_u32(&full_bar[stage]);
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-          mbar_expect_tx(fb, AM == A_GATHER ? B_BYTES : STAGE_BYTES);
           const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
           const int kk = kb * BK;
-          if (BMODE == B_W_MN) {
+          if (elect_one_sync()) {
+            mbar_expect_tx(fb, AM == A_GATHER ? B_BYTES : STAGE_BYTES);
+            if (BMODE == B_W_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_3d(&tma_b, fb, sb + j * 8192, (int)tl.n0 + 64 * j, kk, tl.e);
-          } else if (BMODE == B_W_K) {
-            tma_load_3d(&tma_b, fb, sb, kk, (int)tl.n0, tl.e);
-          } else {
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d(&tma_b, fb, sb + j * 8192, (int)tl.n0 + 64 * j, kk, tl.e);
+            } else if (BMODE == B_W_K) {
+              tma_load_3d(&tma_b, fb, sb, kk, (int)tl.n0, tl.e);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(&tma_b, fb, sb + j * 8192, (int)tl.n0 + 64 * j, (int)(tl.k0 + kk));
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(&tma_b, fb, sb + j * 8192, (int)tl.n0 + 64 * j, (int)(tl.k0 + kk));
+            }
+            if (AM == A_ROWS) {
+              tma_load_2d(&tma_a, fb, sa, kk, (int)tl.m0);
+            } else if (AM == A_MN) {
+              tma_load_2d(&tma_a, fb, sa, (int)tl.m0, (int)(tl.k0 + kk));
+              tma_load_2d(&tma_a, fb, sa + 8192, (int)tl.m0 + 64, (int)(tl.k0 + kk));
+            }
           }
-          if (AM == A_ROWS) {
-            tma_load_2d(&tma_a, fb, sa, kk, (int)tl.m0);
-          } else if (AM == A_MN) {
-            tma_load_2d(&tma_a, fb, sa, (int)tl.m0, (int)(tl.k0 + kk));
-            tma_load_2d(&tma_a, fb, sa + 8192, (int)tl.m0 + 64, (int)(tl.k0 + kk));
-          }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -188,9 +193,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1)
           }
         }
         if (AM == A_GATHER) fence_proxy_async_smem();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(sa_ptr);
-          const uint32_t sb = sa + A_BYTES;
+        const uint32_t sa = smem_u32(sa_ptr);
+        const uint32_t sb = sa + A_BYTES;
+        if (elect_one_sync()) {
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             uint64_t ad, bd;
