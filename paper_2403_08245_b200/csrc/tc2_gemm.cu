@@ -22,6 +22,8 @@
 //   empty[s]  per CTA: the leader's MMAs consumed stage s (multicast commit)
 //   tfull[a]  per CTA: accumulator a complete (multicast commit)
 //   tempty[a] L: both CTAs' epilogues drained accumulator a (16 arrivals)
+#include <atomic>
+
 #include "tc_common.cuh"
 
 namespace smoe {
@@ -30,6 +32,7 @@ namespace tc2 {
 using namespace smoe::tc;
 
 constexpr int TM = 256, TN = 256, BK = 64;
+constexpr int RING = 4;  // tile-id ring entries (dynamic schedule)
 // Epilogue styles (template STAGED):
 //   direct : each thread stores its own accumulator row (7-stage ring);
 //   staged : rows go through a per-warp 4 KB smem tile (6-stage ring) and leave
@@ -71,6 +74,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   constexpr int WM = WP + 1;
   // cp.async data cannot signal the leader's barrier: gather mode relays it
   constexpr bool RELAY = (AM == A_GATHER);
+  // Warps that read every tile id from the ring: both CTAs' epilogue (and
+  // gather) warps, the leader's MMA warp, the peer's producer, and the peer's
+  // relay / bin-tail fixer warp.
+  constexpr int RING_READERS = 2 * (EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0)) + 2 + ((RELAY || GK) ? 1 : 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
@@ -83,8 +90,11 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   uint64_t *empty_bar = bars + 2 * STAGES;       // [STAGES]
   uint64_t *tfull_bar = bars + 3 * STAGES;       // [2]
   uint64_t *tempty_bar = bars + 3 * STAGES + 2;  // [2]
-  uint32_t *s_tmem = (uint32_t *)(bars + 3 * STAGES + 4);  // bars[STAGES..2*STAGES) hold the relay signal
-  int64_t *s_start = (int64_t *)(bars + 3 * STAGES + 6);  // [E+1]
+  uint64_t *ring_full = bars + 3 * STAGES + 4;   // [RING] tile id written (both CTAs)
+  uint64_t *ring_empty = ring_full + RING;       // [RING] L: every consumer warp has read it
+  uint32_t *s_tmem = (uint32_t *)(ring_empty + RING);
+  int32_t *s_tile = (int32_t *)(ring_empty + RING + 1);      // [RING] claimed tile ids (-1 = done)
+  int64_t *s_start = (int64_t *)(ring_empty + RING + 1 + RING / 2);  // [E+1]
   int32_t *s_off = (int32_t *)(s_start + p.E + 1);         // [E+1]
 
   const int warp = threadIdx.x >> 5;
@@ -94,7 +104,6 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   const int64_t nN = (p.N + TN - 1) / TN;
   const int64_t mM = (p.M + TM - 1) / TM;
   const int64_t cluster_id = blockIdx.x >> 1;
-  const int64_t num_clusters = gridDim.x >> 1;
 
   for (int i = threadIdx.x; i <= p.E; i += THREADS) s_off[i] = p.offsets[i];
   if (warp == WP && lane == 0) {
@@ -107,6 +116,10 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&tfull_bar[s]), 1);
       mbar_init(smem_u32(&tempty_bar[s]), 2 * EPI_WARPS);
+    }
+    for (int s = 0; s < RING; ++s) {
+      mbar_init(smem_u32(&ring_full[s]), 1);
+      mbar_init(smem_u32(&ring_empty[s]), RING_READERS);
     }
     fence_barrier_init();
   }
@@ -132,13 +145,56 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   const uint32_t tmem_base = *s_tmem;
   const int64_t total = s_start[p.E];
 
+  // ---- dynamic tile schedule -------------------------------------------------
+  // The leader's producer claims tile ids in increasing order from a global
+  // counter and broadcasts each to both CTAs through a RING-entry shared-memory
+  // ring; every role reads the same sequence.  Pairs that run at the same time
+  // therefore hold neighbouring tiles (band raster stays intact), where a static
+  // round-robin schedule lets pairs drift apart by whole waves and turns the
+  // band's L2 reuse into DRAM re-reads.
+  auto next_tile = [&](int it) -> int64_t {  // ring reader (whole warp)
+    const int slot = it & (RING - 1);
+    mbar_wait_acq_cluster(smem_u32(&ring_full[slot]), (uint32_t)(it / RING) & 1u);
+    const int32_t t = *(volatile int32_t *)&s_tile[slot];
+    __syncwarp();
+    if (elect_one_sync()) {
+      if (leader) mbar_arrive(smem_u32(&ring_empty[slot]));
+      else mbar_arrive_release_cluster(smem_u32(&ring_empty[slot]), 0);
+    }
+    return t;
+  };
+  auto claim_tile = [&](int it) -> int64_t {  // leader producer (whole warp)
+    const int slot = it & (RING - 1);
+    mbar_wait(smem_u32(&ring_empty[slot]), ((uint32_t)(it / RING) & 1u) ^ 1u);
+    if (elect_one_sync()) {
+      const uint32_t c = atomicAdd(p.tile_ctr, 1u);
+      const int32_t t = (int64_t)c < total ? (int32_t)c : -1;
+      s_tile[slot] = t;
+      st_cluster_u32(smem_u32(&s_tile[slot]), 1, (uint32_t)t);
+      mbar_arrive(smem_u32(&ring_full[slot]));
+      mbar_arrive_release_cluster(smem_u32(&ring_full[slot]), 1);
+    }
+    __syncwarp();
+    return *(volatile int32_t *)&s_tile[slot];
+  };
+
   if (warp == WP) {
     // ===================== TMA producer (own halves of A and B) =====================
     // Gather mode: lanes 0..TG_ROWS/4-1 also fetch the first TG_ROWS A rows with
     // TMA tile::gather4 (4 rows per instruction), offloading the cp.async warps.
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = cluster_id; t < total; t += num_clusters) {
+    // the leader claims one tile ahead, so the atomic's latency hides behind a tile's loads
+    int64_t t_next = leader ? claim_tile(0) : 0;
+    for (int it = 0;; ++it) {
+      int64_t t;
+      if (leader) {
+        t = t_next;
+        if (t >= 0) t_next = claim_tile(it + 1);
+      } else {
+        t = next_tile(it);
+      }
+      if (t < 0) break;
       const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
       const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
       const int n_half = (int)(tl.n0 + HN * rank);
@@ -222,7 +278,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       uint32_t acc_phase = 0;
       // p.timing: per-cluster cycle counters of the issue loop (SMOE_TC_TIMING=1, debug)
       long long c_start = clock64(), c_tempty = 0, c_lfull = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         if (tl.nkb == 0) continue;
         long long c0 = p.timing ? clock64() : 0;
@@ -281,7 +339,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       // parity is tracked separately.
       int stage = 0;
       uint32_t parity_bits = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           const int valid = (int)(tl.k_len - (int64_t)kb * BK);
@@ -301,7 +361,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       // ===================== relay (peer CTA, gather mode): own stage landed -> leader =====================
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
@@ -332,7 +394,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       const bool tma_out = GK || p.grouped_out;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         const int64_t row = tl.m0 + HM * rank + r;
         const int64_t slab0 = tl.m0 + HM * rank + q * 32;
@@ -432,7 +496,9 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
       const int r = q * 32 + lane;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = cluster_id; t < total; t += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         const int64_t row = tl.m0 + HM * rank + r;
         const bool valid = row < tl.m_end;
@@ -497,21 +563,32 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
     const int g = threadIdx.x - 32 * EPI_WARPS;
     const int chunk = g & 7;
     const int rsub = g >> 3;
-    // Row indices of the NEXT tile are fetched while this tile streams, so no
-    // index-load latency bubble sits at tile boundaries.
-    auto load_rows = [&](int64_t t, int32_t (&dst)[G_RPT]) {
-      const Tile tn = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+    // Row indices of the NEXT tile are fetched while this tile streams (after
+    // its first stage is issued), so no index-load bubble sits at tile boundaries.
+    auto load_rows = [&](const Tile &tn, int32_t (&dst)[G_RPT]) {
       const int64_t mh = tn.m0 + HM * rank;
 #pragma unroll
       for (int j = 0; j < G_RPT; ++j) dst[j] = __ldg(p.order + min(mh + TG_ROWS + j * G_RSTEP + rsub, tn.m_end - 1));
     };
-    int32_t cur[G_RPT] = {}, nxt[G_RPT] = {};
-    if (cluster_id < total) load_rows(cluster_id, cur);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = cluster_id; t < total; t += num_clusters) {
-      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
-      if (t + num_clusters < total) load_rows(t + num_clusters, nxt);
+    int64_t t = next_tile(0);
+    Tile tl{};
+    int32_t cur[G_RPT] = {}, nxt[G_RPT] = {};
+    if (t >= 0) {
+      tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      load_rows(tl, cur);
+    }
+    for (int it = 0; t >= 0; ++it) {
+      int64_t t_n = -1;
+      Tile tl_n{};
+      auto prefetch_next = [&]() {
+        t_n = next_tile(it + 1);
+        if (t_n >= 0) {
+          tl_n = decode_tile<GK, TM, TN>(t_n, p, s_start, s_off, nN, mM);
+          load_rows(tl_n, nxt);
+        }
+      };
       const __nv_bfloat16 *src[G_RPT];
 #pragma unroll
       for (int j = 0; j < G_RPT; ++j) src[j] = p.x + (int64_t)(cur[j] / p.fan_out) * p.K + chunk * 8;
@@ -528,7 +605,11 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         }
         cp_async_arrive_noinc(smem_u32(&lfull_bar[stage]));
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (kb == 0) prefetch_next();
       }
+      if (tl.nkb == 0) prefetch_next();
+      t = t_n;
+      tl = tl_n;
 #pragma unroll
       for (int j = 0; j < G_RPT; ++j) cur[j] = nxt[j];
     }
@@ -558,7 +639,8 @@ static int group_m_k_setting() {
 
 static size_t smem_bytes(int E, bool staged) {
   const int stages = ring_stages(staged);
-  return 1024 + stages * STAGE_BYTES + (staged ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 6) + 12 * (E + 1) + 64;
+  return 1024 + stages * STAGE_BYTES + (staged ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 4 + 2 * RING + 2 + RING / 2) +
+         12 * (E + 1) + 64;
 }
 
 }  // namespace tc2
@@ -568,6 +650,20 @@ bool tc2_supports_experts(int E) {
 }
 
 namespace tc2 {
+
+// Tile counters of the dynamic schedule: one zeroed (stream-ordered memset) per
+// launch; a 64-entry pool so launches in flight on different streams never
+// share one.
+__device__ uint32_t g_tile_ctr[64];
+
+static uint32_t *tile_counter(cudaStream_t st) {
+  static uint32_t *base = nullptr;
+  static std::atomic<unsigned> seq{0};
+  if (!base && cudaGetSymbolAddress((void **)&base, g_tile_ctr) != cudaSuccess) return nullptr;
+  uint32_t *c = base + (seq.fetch_add(1) % 64);
+  if (cudaMemsetAsync(c, 0, sizeof(uint32_t), st) != cudaSuccess) return nullptr;
+  return c;
+}
 
 template <int AM, int BMODE, bool GK, bool STAGED>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &tc, const CUtensorMap &tc2,
@@ -582,7 +678,10 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   }
   int clusters = num_sms() / 2;
   if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
-  kern<<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, tc, tc2, p);
+  Params q = p;
+  q.tile_ctr = tile_counter(st);
+  if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
+  kern<<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, tc, tc2, q);
   return check_launch("tc2_gemm");
 }
 

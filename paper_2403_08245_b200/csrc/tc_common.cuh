@@ -29,6 +29,7 @@ struct Params {
   const __nv_bfloat16 *x;  // A_GATHER: the scattered input rows [x_rows, K]
   int group_m;             // m-blocks per raster band
   int timing;              // debug: print issue-loop wait counters (SMOE_TC_TIMING)
+  uint32_t *tile_ctr;      // CTA-pair kernels: zeroed global counter tiles are claimed from (in order)
 };
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -154,6 +155,39 @@ __device__ __forceinline__ bool elect_one_sync() {
 }
 
 // ---- cluster helpers (2-CTA pairs) ---------------------------------------------
+// wait with cluster-scope acquire (data written by the peer CTA before its
+// release-arrive on this barrier is visible afterwards)
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// release-arrive (cluster scope) on the barrier at this offset in CTA `cta`
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t local_bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(local_bar),
+      "r"(cta)
+      : "memory");
+}
+// 32-bit store into the same shared offset of CTA `cta`
+__device__ __forceinline__ void st_cluster_u32(uint32_t local_addr, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(local_addr),
+      "r"(cta), "r"(v)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

@@ -50,6 +50,8 @@ for _ in range(3):
             r_al = sm.RoutingResult(ids_al, routing.p, routing.gate_full, renormalized=True, validate=False)
             order_al = sm.compute_grouped_order(r_al)
         sm.group_xty(h, xg, order_al)
+    elif which == "cublas":  # dense library GEMM with the same FLOPs (n x d @ d x d_e)
+        torch.matmul(xg, w[0])
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()
