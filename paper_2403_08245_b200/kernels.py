@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
+from . import launch_timer as _lt
 from .errors import require_dims
 from .router import GroupedOrder
 
@@ -140,6 +141,14 @@ def _engine_id(engine: str | None) -> int:
     return _lib.ENGINE_IDS[engine or _engine]
 
 
+def _s2s_label(layout: LayoutFlag, transpose_w: bool, epi: int) -> str:
+    lab = "scatter2scatter " + ("G" if layout.grouped_in else "S") + "->" + ("G" if layout.grouped_out else "S")
+    if transpose_w:
+        lab += " W^T"
+    return lab + {_lib.EPI_NONE: "", _lib.EPI_ACT: " +act(pre,post)", _lib.EPI_ACT_GRAD: " *act'",
+                  _lib.EPI_ACT_ONLY: " +act"}.get(epi, "")
+
+
 # ---- kernels ---------------------------------------------------------------------
 
 def scatter2scatter(
@@ -212,11 +221,13 @@ def scatter2scatter(
                          tuple(act_grad_of.shape), (num_slots, d_out))
             aux = _cuda(act_grad_of, "act_grad_of")
     lib = _lib.load()
+    t0 = _lt.begin()
     st = lib.smoe_scatter2scatter(
         x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], w.shape[1], w.shape[2],
         order.o.data_ptr(), order.bin_offsets.data_ptr(), num_slots, fan_out,
         int(layout.grouped_in), int(layout.grouped_out), int(transpose_w), _dtype_id(x), epi, act_id,
         out.data_ptr(), _ptr(act_out), _ptr(aux), _engine_id(engine), _stream(x))
+    _lt.end(_s2s_label(layout, transpose_w, epi), t0)
     _lib.check(st, "scatter2scatter")
     _credit(order, d_in, d_out)
     if _fault_inject and out.numel():
@@ -257,10 +268,12 @@ def scatter_combine(
     rows = num_slots // combine_cols
     acc = torch.empty((rows, d_out), dtype=torch.float32, device=x.device)
     y = acc if x.dtype == torch.float32 else torch.empty((rows, d_out), dtype=x.dtype, device=x.device)
+    t0 = _lt.begin()
     st = _lib.load().smoe_scatter_combine(
         x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], d_in, d_out, order.o.data_ptr(),
         order.bin_offsets.data_ptr(), num_slots, fan_out, p32.data_ptr(), combine_cols, int(grouped_in),
         _dtype_id(x), acc.data_ptr(), y.data_ptr(), _stream(x))
+    _lt.end("scatter_combine " + ("G" if grouped_in else "S") + "->combine", t0)
     _lib.check(st, "scatter_combine")
     _credit(order, d_in, d_out)
     return y
@@ -290,8 +303,10 @@ def group(
                      (num_slots, x.shape[1]))
         if out.dtype != x.dtype:
             raise ValueError(f"out dtype {out.dtype} does not match input dtype {x.dtype}")
+    t0 = _lt.begin()
     st = _lib.load().smoe_group(x.data_ptr(), x.shape[0], x.shape[1], order.o.data_ptr(), num_slots,
                                 fan_out, _ptr(weights), _dtype_id(x), out.data_ptr(), _stream(x))
+    _lt.end("group", t0)
     _lib.check(st, "group")
     return out
 
@@ -318,9 +333,11 @@ def group_xty(
         out = torch.empty((e, d_in, d_out), dtype=xg.dtype, device=xg.device)
     else:
         require_dims(tuple(out.shape) == (e, d_in, d_out), "dw buffer", tuple(out.shape), (e, d_in, d_out))
+    t0 = _lt.begin()
     st = _lib.load().smoe_group_xty(xg.data_ptr(), yg.data_ptr(), order.bin_offsets.data_ptr(), e,
                                     num_slots, d_in, d_out, _dtype_id(xg), out.data_ptr(),
                                     _engine_id(engine), _stream(xg))
+    _lt.end("group_xty", t0)
     _lib.check(st, "group_xty")
     _credit(order, d_in, d_out)
     return out
@@ -335,8 +352,10 @@ def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = Non
     p32 = _cuda(p.to(torch.float32), "p")
     if out is None:
         out = torch.empty((s, y_hat.shape[1]), dtype=y_hat.dtype, device=y_hat.device)
+    t0 = _lt.begin()
     st = _lib.load().smoe_combine(y_hat.data_ptr(), p32.data_ptr(), s, j, y_hat.shape[1],
                                   _dtype_id(y_hat), out.data_ptr(), _stream(y_hat))
+    _lt.end("combine", t0)
     _lib.check(st, "combine")
     return out
 
@@ -345,8 +364,10 @@ def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int) -> tor
     """dp[s, i] = <dY[s], Y_hat[s*j + i]>  (parallel_linear.py:198-206), float32."""
     dy, y_hat = _cuda(dy, "dy"), _cuda(y_hat, "y_hat")
     dp = torch.empty((s, j), dtype=torch.float32, device=dy.device)
+    t0 = _lt.begin()
     st = _lib.load().smoe_combine_grad_p(dy.data_ptr(), y_hat.data_ptr(), s, j, dy.shape[1],
                                          _dtype_id(dy), dp.data_ptr(), _stream(dy))
+    _lt.end("combine_grad_p", t0)
     _lib.check(st, "combine_grad_p")
     return dp
 
@@ -357,8 +378,10 @@ def fanout_reduce(slot_grads: torch.Tensor, fan_out: int, out: torch.Tensor | No
     t = g.shape[0] // fan_out
     if out is None:
         out = torch.empty((t, g.shape[1]), dtype=g.dtype, device=g.device)
+    t0 = _lt.begin()
     st = _lib.load().smoe_fanout_reduce(g.data_ptr(), t, fan_out, g.shape[1], _dtype_id(g),
                                         out.data_ptr(), _stream(g))
+    _lt.end("fanout_reduce", t0)
     _lib.check(st, "fanout_reduce")
     return out
 
@@ -371,7 +394,9 @@ def activation_kernel(x: torch.Tensor, name: str, derivative: bool,
     x = _cuda(x, "x")
     if out is None:
         out = torch.empty_like(x)
+    t0 = _lt.begin()
     st = _lib.load().smoe_apply_activation(x.data_ptr(), x.numel(), _lib.ACTIVATION_IDS[name],
                                            int(derivative), _dtype_id(x), out.data_ptr(), _stream(x))
+    _lt.end("activation", t0)
     _lib.check(st, "activation")
     return out

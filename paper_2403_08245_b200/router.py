@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
+from . import launch_timer as _lt
 from .errors import require_dims
 
 
@@ -156,9 +157,11 @@ def _sort_ids(flat_ids: torch.Tensor, num_experts: int):
     ws_bytes = lib.smoe_route_sort_workspace_bytes(n, num_experts)
     ws = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
+        t0 = _lt.begin()
         st = lib.smoe_route_sort(ids.data_ptr(), n, num_experts, o.data_ptr(), sorted_ids.data_ptr(),
                                  offsets.data_ptr(), inv.data_ptr(), ws.data_ptr(), ws_bytes,
                                  _stream_ptr(dev))
+        _lt.end("route_sort", t0)
     _lib.check(st, "compute_grouped_order")
     return o, sorted_ids, offsets, inv
 
@@ -214,9 +217,11 @@ def _router_kernel(inp: torch.Tensor, k: int, renormalize: bool, apply_softmax: 
     idx = torch.empty((t, k), dtype=torch.int64, device=inp.device)
     p = torch.empty((t, k), dtype=torch.float32, device=inp.device)
     gate = torch.empty_like(inp) if apply_softmax else inp
+    t0 = _lt.begin()
     st = _lib.load().smoe_router_topk(inp.data_ptr(), t, e, k, int(apply_softmax), int(renormalize),
                                       gate.data_ptr() if apply_softmax else None, idx.data_ptr(), p.data_ptr(),
                                       _stream_ptr(inp.device))
+    _lt.end("router_topk", t0)
     _lib.check(st, "router_topk")
     return gate, idx, p
 
