@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SMOE_ABI_VERSION 1
+#define SMOE_ABI_VERSION 2
 
 typedef enum {
   SMOE_OK = 0,
@@ -157,12 +157,17 @@ int smoe_apply_activation(const void *x, int64_t numel, int32_t activation, int3
  *   y_accum [n / combine_cols, d_out] float32, zeroed by this call.
  *   y       [n / combine_cols, d_out] dtype (rounded copy of y_accum; may be
  *           the same buffer as y_accum when dtype == SMOE_F32).
+ *   engine  SMOE_ENGINE_AUTO: bf16 runs the tcgen05 CTA-pair GEMM whose
+ *           epilogue scales each row by p and adds it into y_accum with fp32
+ *           vector reductions (order of the k additions per token is not
+ *           fixed: bit-reproducible for k <= 2, within fp32 rounding above);
+ *           fp32 and unsupported shapes run the SIMT kernel.
  */
 int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
                          int64_t d_in, int64_t d_out, const int32_t *order,
                          const int32_t *expert_offsets, int64_t n, int32_t fan_out,
                          const float *p_flat, int32_t combine_cols, int32_t grouped_in,
-                         int32_t dtype, float *y_accum, void *y, void *stream);
+                         int32_t dtype, float *y_accum, void *y, int32_t engine, void *stream);
 
 #ifdef __cplusplus
 }

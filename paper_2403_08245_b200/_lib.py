@@ -45,7 +45,7 @@ SIGNATURES = {
     "smoe_fanout_reduce": (_c.c_int, [_vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_apply_activation": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "smoe_scatter_combine": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
-                                        _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+                                        _vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
 }
 
 _lib = None
@@ -54,6 +54,9 @@ _load_error: str | None = None
 
 class LibraryError(RuntimeError):
     """The native library is missing or a native call failed."""
+
+
+ABI_VERSION = 2  # include/smoe_b200.h SMOE_ABI_VERSION
 
 
 def load(path: str | os.PathLike | None = None):
@@ -70,7 +73,7 @@ def load(path: str | os.PathLike | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.smoe_abi_version() != 1:
+    if lib.smoe_abi_version() != ABI_VERSION:
         raise LibraryError("libsmoe_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -41,6 +41,10 @@ bool tc_available();
 bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out);
 int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int tc_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+bool tc_supports_combine(int, int64_t, int64_t, const void *, const void *, const void *);
+int tc_scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
+                       int64_t, int, int, const float *, int, float *, cudaStream_t);
+int round_copy(const float *, int64_t, int, void *, cudaStream_t);
 
 }  // namespace smoe
 
@@ -193,7 +197,7 @@ int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t n
                          int64_t d_in, int64_t d_out, const int32_t *order,
                          const int32_t *expert_offsets, int64_t n, int32_t fan_out,
                          const float *p_flat, int32_t combine_cols, int32_t grouped_in,
-                         int32_t dtype, float *y_accum, void *y, void *stream) {
+                         int32_t dtype, float *y_accum, void *y, int32_t engine, void *stream) {
   REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
   REQUIRE(combine_cols >= 1 && n % combine_cols == 0, SMOE_EINVAL,
           "combine width " + std::to_string(combine_cols) + " must divide T*k (" + std::to_string(n) + ")");
@@ -203,6 +207,20 @@ int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t n
   else
     REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
   REQUIRE(y_accum && y, SMOE_EINVAL, "scatter_combine: null output");
+  if (n == 0 || d_out == 0) return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n,
+                                                        fan_out, p_flat, combine_cols, grouped_in, dtype, y_accum, y,
+                                                        S(stream));
+  REQUIRE(x && w && order && expert_offsets && p_flat, SMOE_EINVAL, "scatter_combine: null pointer");
+  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
+                      (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() &&
+                       tc_supports_combine(num_experts, d_in, d_out, x, w, y_accum));
+  if (use_tc) {
+    REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
+    int st = tc_scatter_combine(x, x_rows, w, num_experts, d_in, d_out, order, expert_offsets, n, fan_out, grouped_in,
+                                p_flat, combine_cols, y_accum, S(stream));
+    if (st != SMOE_OK) return st;
+    return round_copy(y_accum, (n / combine_cols) * d_out, dtype, y, S(stream));
+  }
   return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n, fan_out, p_flat,
                               combine_cols, grouped_in, dtype, y_accum, y, S(stream));
 }

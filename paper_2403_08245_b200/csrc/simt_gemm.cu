@@ -249,6 +249,18 @@ int simt_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E
   return check_launch("simt_group_xty");
 }
 
+// y = round(y_accum) (bf16), or a no-op when y aliases the fp32 accumulator.
+int round_copy(const float *y_accum, int64_t numel, int dtype, void *y, cudaStream_t st) {
+  if (numel <= 0 || (const void *)y == (const void *)y_accum) return SMOE_OK;
+  int64_t b = (numel + 255) / 256;
+  unsigned blocks = (unsigned)(b < 148 * 16 ? b : 148 * 16);
+  if (dtype == SMOE_BF16)
+    round_copy_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(y_accum, numel, (__nv_bfloat16 *)y);
+  else
+    round_copy_kernel<float><<<blocks, 256, 0, st>>>(y_accum, numel, (float *)y);
+  return check_launch("round_copy");
+}
+
 int simt_scatter_combine(const void *x, const void *w, int E, int64_t d_in, int64_t d_out,
                          const int32_t *order, const int32_t *offsets, int64_t n, int fan_out,
                          const float *p_flat, int combine_cols, int gin, int dtype,

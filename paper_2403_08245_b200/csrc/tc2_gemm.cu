@@ -408,6 +408,13 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         long long cdst[8];
   #pragma unroll
         for (int i = 0; i < 8; ++i) cdst[i] = __shfl_sync(0xffffffffu, dst, cr + 4 * i);
+        const bool combine = p.epi == EPI_COMBINE;
+        float cscale = 0.f;  // combine: this thread's row weight; cdst becomes the token row
+        if (combine) {
+          if (dst >= 0) cscale = __ldg(p.pw + dst);
+  #pragma unroll
+          for (int i = 0; i < 8; ++i) cdst[i] = cdst[i] >= 0 ? cdst[i] / p.combine_cols : -1;
+        }
         const bool has_acc = tl.nkb > 0;
         if (has_acc) {
           mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
@@ -422,6 +429,39 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
           // the staging tile is reused: the previous TMA store must have read it
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
+          if (combine) {
+            // p-scaled fp32 rows -> staging tile (32 rows x 32 columns x 4 B per
+            // half) -> coalesced 16-byte vector reductions into the token rows
+  #pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t v[32];
+              if (has_acc) {
+                tmem_ld16(tbase + cg + 32 * hf, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(tbase + cg + 32 * hf + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld_wait();
+              } else {
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0u;
+              }
+  #pragma unroll
+              for (int c = 0; c < 8; ++c)
+                sts128(stg + lane * 128 + ((c ^ (lane & 7)) << 4),
+                       make_uint4(__float_as_uint(__uint_as_float(v[4 * c]) * cscale),
+                                  __float_as_uint(__uint_as_float(v[4 * c + 1]) * cscale),
+                                  __float_as_uint(__uint_as_float(v[4 * c + 2]) * cscale),
+                                  __float_as_uint(__uint_as_float(v[4 * c + 3]) * cscale)));
+              __syncwarp();
+              const int64_t ccol = col0 + 32 * hf + cc * 4;
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rl = cr + 4 * i;
+                const uint4 val = lds128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4));
+                if (cdst[i] >= 0 && ccol < p.N) red_add_v4(p.yacc + cdst[i] * p.N + ccol, val);
+              }
+              __syncwarp();
+            }
+            continue;
+          }
           if (p.epi == SMOE_EPI_ACT_GRAD) {
             // coalesced read of the 32 rows' h_pre segments into the staging tile
   #pragma unroll
@@ -721,9 +761,10 @@ static bool encode_out_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_
   return encode_map(m, ptr, 2, dims, strides, box);
 }
 
-int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
                     const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout, int trans,
-                    int epi, int act, void *out, void *out2, const void *aux, cudaStream_t st) {
+                    int epi, int act, void *out, void *out2, const void *aux, const float *pw, float *yacc,
+                    int combine_cols, cudaStream_t st) {
   const int64_t d_in = trans ? w_cols : w_rows;
   const int64_t d_out = trans ? w_rows : w_cols;
   CUtensorMap ta, tb;
@@ -754,6 +795,9 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.out2 = (epi == SMOE_EPI_ACT) ? (__nv_bfloat16 *)out2 : nullptr;
   p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
   p.x = (const __nv_bfloat16 *)x;
+  p.pw = pw;
+  p.yacc = yacc;
+  p.combine_cols = combine_cols;
   p.group_m = band_rows(d_in);
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
@@ -763,7 +807,7 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
-    if (staged_for(false, gout)) {
+    if (epi == EPI_COMBINE || staged_for(false, gout)) {
       if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
       return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
     }
@@ -772,6 +816,24 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
   }
   if (!trans) return launch<A_GATHER, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
   return launch<A_GATHER, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
+}
+
+int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                    const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout, int trans,
+                    int epi, int act, void *out, void *out2, const void *aux, cudaStream_t st) {
+  return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi, act, out, out2,
+                  aux, nullptr, nullptr, 1, st);
+}
+
+// scatter_combine (kernels.py:242-286): scattered-output GEMM whose epilogue
+// adds p_flat[slot] * row into yacc[slot / combine_cols] (fp32, zeroed here).
+int scatter_combine(const void *x, int64_t x_rows, const void *w, int E, int64_t d_in, int64_t d_out,
+                    const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, const float *p_flat,
+                    int combine_cols, float *yacc, cudaStream_t st) {
+  if (cudaMemsetAsync(yacc, 0, sizeof(float) * (n / combine_cols) * d_out, st) != cudaSuccess)
+    return check_launch("scatter_combine: zero accumulator");
+  return s2s_impl(x, x_rows, w, E, d_in, d_out, order, offsets, n, fan_out, gin, 0, 0, EPI_COMBINE, 0, yacc,
+                  nullptr, nullptr, p_flat, yacc, combine_cols, st);
 }
 
 int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in, int64_t d_out,

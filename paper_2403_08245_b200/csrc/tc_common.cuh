@@ -11,6 +11,10 @@ namespace tc {
 
 enum AMode { A_ROWS = 0, A_GATHER = 1, A_MN = 2 };
 enum BMode { B_W_MN = 0, B_W_K = 1, B_ROWS_MN = 2 };
+// Internal epilogue (smoe_scatter_combine, not a public SMOE_EPI_* value): each
+// accumulator row is scaled by its slot's combine weight and added into the
+// fp32 token row yacc[order[i] / combine_cols] (vector reductions in L2).
+constexpr int EPI_COMBINE = 16;
 
 struct Params {
   int E;
@@ -30,6 +34,9 @@ struct Params {
   int group_m;             // m-blocks per raster band
   int timing;              // debug: print issue-loop wait counters (SMOE_TC_TIMING)
   uint32_t *tile_ctr;      // CTA-pair kernels: zeroed global counter tiles are claimed from (in order)
+  const float *pw;         // EPI_COMBINE: combine weight per scattered slot
+  float *yacc;             // EPI_COMBINE: fp32 [n / combine_cols, N] accumulator
+  int combine_cols;        // EPI_COMBINE: slots per output row
 };
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -406,6 +413,12 @@ __device__ __forceinline__ void bulk_signal_cta0(uint32_t dst_local, uint32_t sr
 // ---- staged epilogue helpers (CTA-pair kernel) -----------------------------------
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// Fire-and-forget fp32 vector reduction into global memory (performed in L2).
+__device__ __forceinline__ void red_add_v4(float *addr, uint4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
                : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {

@@ -402,6 +402,8 @@ namespace tc2 {
 int scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
                     int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+int scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
+                    int64_t, int, int, const float *, int, float *, cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -472,6 +474,21 @@ int tc_scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int6
   }
   if (!trans) return launch<A_GATHER, B_W_MN, false>(ta, tb, p, max_tiles, st);
   return launch<A_GATHER, B_W_K, false>(ta, tb, p, max_tiles, st);
+}
+
+// The combine epilogue exists in the CTA-pair kernels only.
+bool tc_supports_combine(int E, int64_t d_in, int64_t d_out, const void *x, const void *w, const void *yacc) {
+  return tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && tc_supports_s2s(d_in, d_out, x, w, yacc);
+}
+
+int tc_scatter_combine(const void *x, int64_t x_rows, const void *w, int E, int64_t d_in, int64_t d_out,
+                       const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin,
+                       const float *p_flat, int combine_cols, float *yacc, cudaStream_t st) {
+  if (!tc_supports_combine(E, d_in, d_out, x, w, yacc))
+    return fail(SMOE_ENOTSUP, "tcgen05 scatter_combine needs the CTA-pair engine, d_in, d_out multiples of 8 and "
+                              "16-byte aligned buffers");
+  return tc2::scatter_combine(x, x_rows, w, E, d_in, d_out, order, offsets, n, fan_out, gin, p_flat, combine_cols,
+                              yacc, st);
 }
 
 int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in,

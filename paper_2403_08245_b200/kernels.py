@@ -244,11 +244,16 @@ def scatter_combine(
     combine_cols: int,
     grouped_in: bool,
     tile: TileConfig | None = None,
+    *,
+    engine: str | None = None,
 ) -> torch.Tensor:
     """scatter2scatter with the weighted slot-sum fused into the write (kernels.py:242-286).
 
     The T*k pre-combine buffer never exists: the per-slot products are scaled by
-    p and accumulated into an fp32 (T, d_out) buffer, then rounded once.
+    p and accumulated into an fp32 (T, d_out) buffer, then rounded once.  bf16
+    runs the tcgen05 GEMM with the scale-and-add in its epilogue (fp32 vector
+    reductions; the k additions per token land in completion order, so results
+    are bit-reproducible for k <= 2 and within fp32 rounding otherwise).
     """
     if fan_out < 1:
         raise ValueError(f"fan_out must be >= 1, got {fan_out}")
@@ -272,7 +277,7 @@ def scatter_combine(
     st = _lib.load().smoe_scatter_combine(
         x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], d_in, d_out, order.o.data_ptr(),
         order.bin_offsets.data_ptr(), num_slots, fan_out, p32.data_ptr(), combine_cols, int(grouped_in),
-        _dtype_id(x), acc.data_ptr(), y.data_ptr(), _stream(x))
+        _dtype_id(x), acc.data_ptr(), y.data_ptr(), _engine_id(engine), _stream(x))
     _lt.end("scatter_combine " + ("G" if grouped_in else "S") + "->combine", t0)
     _lib.check(st, "scatter_combine")
     _credit(order, d_in, d_out)

@@ -170,3 +170,50 @@ def test_row_kernels_bf16():
     assert rel_err(dp, orc.combine_grad_p(dy, y_hat, tokens, k)) <= 1e-4
     dx = sm.kernels.fanout_reduce(yh, k)
     assert rel_err(dx, orc.fanout_reduce(y_hat, k)) <= 1e-2
+
+
+@pytest.mark.parametrize("grouped_in", [False, True])
+@pytest.mark.parametrize("flavor", ["gate", "all_to_one", "skip_one"])
+def test_scatter_combine_bf16_tcgen05(grouped_in, flavor):
+    """Inference combine on the tensor cores (kernels.py:242-286): the GEMM
+    epilogue scales each slot row by p and reduces it into the fp32 token row."""
+    rng = np.random.default_rng(hash(("combine", grouped_in, flavor)) % 2**32)
+    layout = sm.GROUPED_TO_SCATTERED if grouped_in else sm.SCATTERED_TO_SCATTERED
+    for tokens, k, e, d_in, d_out in [(300, 2, 6, 256, 512), (1000, 4, 8, 128, 256), (77, 3, 5, 64, 200)]:
+        idx, x, w, fan_out = _problem(rng, tokens, k, e, d_in, d_out, layout, False, flavor)
+        p = rng.uniform(0.05, 1.0, (tokens, k)).astype(np.float32)
+        xb, wb = bf16_round(x), bf16_round(w)
+        o, off = orc.compute_grouped_order(idx, e)
+        want = orc.scatter_combine(xb, wb, o, off, fan_out, p.reshape(-1), k, grouped_in)
+        order = order_of(idx, e)
+        y = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                               t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+        assert y.dtype == torch.bfloat16 and tuple(y.shape) == (tokens, d_out)
+        assert rel_err(y, want) <= 2e-2, (tokens, k, rel_err(y, want))
+        # same as the SIMT engine within bf16 rounding
+        ys = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                t(p.reshape(-1)), k, grouped_in, engine="simt")
+        assert rel_err(y, np_of(ys)) <= 1e-2
+        if k <= 2:  # two fp32 additions into a zeroed row commute: bit-reproducible
+            y2 = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                    t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+            assert torch.equal(y, y2)
+
+
+def test_inference_mlp_uses_tcgen05_combine():
+    """smoe_mlp_forward(training=False) at a C1-like shape: the layer-2 combine
+    runs on the tensor cores and matches the training path's combine."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    tokens, d, de, e, k = 4096, 1024, 2048, 8, 2
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / de ** 0.5).to(torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+    order = sm.compute_grouped_order(routing)
+    from paper_2403_08245_b200.launch_timer import LaunchTimer
+    with LaunchTimer() as lt:
+        y_inf, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=False)
+    labels = list(lt.summary())
+    assert any(lab.startswith("scatter_combine") for lab in labels), labels
+    y_tr, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=True)
+    assert rel_err(y_inf, np_of(y_tr)) <= 1e-2
