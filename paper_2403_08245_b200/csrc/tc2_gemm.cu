@@ -730,13 +730,19 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
 // (base-clock ncu, C1: rows 88.2 -> 86.8 %, dh 81.0 -> 79.7 %, xty 70.1 -> 69.3 %
 // tensor-pipe active when staged; gather 75.0 -> 77.0 %, l1 68.4 -> 70.6 %).
 // SMOE_TC_EPI=all stages every grouped-output kernel too (A/B experiments).
-static bool staged_for(bool gather, bool grouped_out) {
+// Short-K GEMMs (K <= SMOE_TC_STAGE_K, default 1024: the MoMHA projections'
+// d_proj = 512 side) are epilogue-bound, so they stage too: a tile's mainloop
+// is only K/64 ring stages long and the 7th stage buys nothing.
+static bool staged_for(bool gather, bool grouped_out, int64_t K) {
   static int all = -1;
+  static int64_t small_k = -1;
   if (all < 0) {
     const char *env = getenv("SMOE_TC_EPI");
     all = (env && !strcmp(env, "all")) ? 1 : 0;
+    const char *k = getenv("SMOE_TC_STAGE_K");
+    small_k = k ? atoll(k) : 1024;
   }
-  return gather || (all && grouped_out);
+  return gather || (all && grouped_out) || K <= small_k;
 }
 
 // Row-blocks (256 rows) per raster band of the grouped-M schedule.  With the
@@ -807,7 +813,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
-    if (epi == EPI_COMBINE || staged_for(false, gout)) {
+    if (epi == EPI_COMBINE || staged_for(false, gout, d_in)) {
       if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
       return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
     }
@@ -867,7 +873,7 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
   CUtensorMap tc;
   if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
-  if (staged_for(false, true)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);
+  if (staged_for(false, true, INT64_MAX)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);
   return launch<A_MN, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
 }
 

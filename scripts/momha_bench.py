@@ -61,13 +61,20 @@ def main():
         sm.momha_backward(ctx, dy)
 
     ms_proj = timed(projections)
+    from paper_2403_08245_b200.launch_timer import LaunchTimer
+    with LaunchTimer() as lt:
+        for _ in range(5):
+            projections()
+    kern = {lab: {"ms_per_launch": v["ms_per_launch"], "launches_per_step": v["launches"] / 5}
+            for lab, v in lt.summary().items()}
     ms_layer = timed(layer, steps=5, warmup=2)
     flops = 12.0 * t * k * d * dp_
     line = {
         "workload": "C3 MoMHA: B=8 x seq 4096 (T=32768), E=16, k=4, d_model=2048, d_head=128, d_proj=512, causal, bf16",
         "projections": {"ms_per_step": ms_proj, "tokens_per_s": t / (ms_proj / 1e3),
                         "tflops": flops / (ms_proj / 1e3) / 1e12, "flop_per_step": flops,
-                        "what": "ParallelLinear q (S->S, fan-out 4) + o (S->S, gate combine), fwd+bwd"},
+                        "what": "ParallelLinear q (S->S, fan-out 4) + o (S->S, gate combine), fwd+bwd",
+                        "kernels": kern},
         "layer": {"ms_per_step": ms_layer, "tokens_per_s": t / (ms_layer / 1e3),
                   "what": "momha_forward + momha_backward (projections, shared K/V GEMMs, fused SDPA core)"},
         "launches_note": "projection kernels from libsmoe_b200.so; K/V GEMMs and SDPA are torch library kernels",
