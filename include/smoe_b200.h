@@ -152,6 +152,19 @@ int smoe_apply_activation(const void *x, int64_t numel, int32_t activation, int3
                     int32_t dtype, void *out, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * group_xty over scattered operands: the reference's group() + group_xty()
+ * pair (parallel_linear.py:224-234, kernels.py:289-361) with the grouped copies
+ * never materialised.  dw[e] = Xb[bin e]^T @ Yb[bin e] where grouped position i
+ * of Xb is x[i] when x_grouped else x[order[i] / x_fan_out] (same for y).
+ *   x [x_rows, d_in], y [y_rows, d_out]; x_rows = n (grouped) or n / x_fan_out.
+ */
+int smoe_group_xty_scattered(const void *x, int64_t x_rows, int32_t x_fan_out, int32_t x_grouped,
+                             const void *y, int64_t y_rows, int32_t y_fan_out, int32_t y_grouped,
+                             const int32_t *order, const int32_t *expert_offsets, int32_t num_experts,
+                             int64_t n, int64_t d_in, int64_t d_out, int32_t dtype, void *dw,
+                             int32_t engine, void *stream);
+
+/* ---------------------------------------------------------------------------
  * scatter_combine (kernels.py:242-286), inference: y[order[i] / combine_cols] +=
  *   p_flat[order[i]] * (x[src] @ W[e]) with no T*k buffer.
  *   y_accum [n / combine_cols, d_out] float32, zeroed by this call.

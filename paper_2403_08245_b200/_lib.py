@@ -44,6 +44,8 @@ SIGNATURES = {
     "smoe_combine_grad_p": (_c.c_int, [_vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_fanout_reduce": (_c.c_int, [_vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_apply_activation": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_group_xty_scattered": (_c.c_int, [_vp, _i64, _i32, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i64,
+                                            _i64, _i64, _i32, _vp, _i32, _vp]),
     "smoe_scatter_combine": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
                                         _vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
 }

@@ -45,6 +45,11 @@ bool tc_supports_combine(int, int64_t, int64_t, const void *, const void *, cons
 int tc_scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
                        int64_t, int, int, const float *, int, float *, cudaStream_t);
 int round_copy(const float *, int64_t, int, void *, cudaStream_t);
+bool tc_supports_xty_scattered(int, int64_t, int64_t, int64_t, int64_t, const void *, const void *, const void *);
+int tc_group_xty_scattered(const void *, int64_t, int, int, const void *, int64_t, int, int, const int32_t *,
+                           const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+int simt_group_xty_scattered(const void *, int, int, const void *, int, int, const int32_t *, const int32_t *, int,
+                             int64_t, int64_t, int, void *, cudaStream_t);
 
 }  // namespace smoe
 
@@ -126,6 +131,31 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
   }
   return simt_scatter2scatter(x, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out, grouped_in,
                               grouped_out, transpose_w, dtype, epilogue, activation, out, out2, aux, S(stream));
+}
+
+int smoe_group_xty_scattered(const void *x, int64_t x_rows, int32_t x_fan_out, int32_t x_grouped, const void *y,
+                             int64_t y_rows, int32_t y_fan_out, int32_t y_grouped, const int32_t *order,
+                             const int32_t *expert_offsets, int32_t num_experts, int64_t n, int64_t d_in,
+                             int64_t d_out, int32_t dtype, void *dw, int32_t engine, void *stream) {
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype " + std::to_string(dtype));
+  REQUIRE(num_experts >= 1, SMOE_EINVAL, "num_experts must be >= 1");
+  REQUIRE(x_fan_out >= 1 && y_fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
+  REQUIRE(dw && expert_offsets, SMOE_EINVAL, "group_xty_scattered: null pointer");
+  REQUIRE(n == 0 || (x && y && order), SMOE_EINVAL, "group_xty_scattered: null pointer");
+  REQUIRE(x_grouped ? x_rows == n : x_rows * x_fan_out == n, SMOE_ESHAPE,
+          "x rows (" + std::to_string(x_rows) + ") do not cover the " + std::to_string(n) + " slots");
+  REQUIRE(y_grouped ? y_rows == n : y_rows * y_fan_out == n, SMOE_ESHAPE,
+          "y rows (" + std::to_string(y_rows) + ") do not cover the " + std::to_string(n) + " slots");
+  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
+                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && n > 0 &&
+                 tc_supports_xty_scattered(num_experts, x_rows, d_in, y_rows, d_out, x, y, dw));
+  if (use_tc) {
+    REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
+    return tc_group_xty_scattered(x, x_rows, x_fan_out, x_grouped, y, y_rows, y_fan_out, y_grouped, order,
+                                  expert_offsets, num_experts, n, d_in, d_out, dw, S(stream));
+  }
+  return simt_group_xty_scattered(x, x_fan_out, x_grouped, y, y_fan_out, y_grouped, order, expert_offsets,
+                                  num_experts, d_in, d_out, dtype, dw, S(stream));
 }
 
 int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets,

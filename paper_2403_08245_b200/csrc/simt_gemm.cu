@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(S_THREADS) simt_xty_kernel(const T *__restrict
                                                              const T *__restrict__ yg,
                                                              const int32_t *__restrict__ offsets,
                                                              int64_t d_in, int64_t d_out,
-                                                             T *__restrict__ dw) {
+                                                             T *__restrict__ dw,
+                                                             const int32_t *__restrict__ order = nullptr,
+                                                             int fa = 1, int ga = 1, int fb = 1, int gb = 1) {
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const int e = blockIdx.z;
@@ -176,8 +178,11 @@ __global__ void __launch_bounds__(S_THREADS) simt_xty_kernel(const T *__restrict
       int kr = idx / SB_M, c = idx % SB_M;
       int64_t r = k0 + kr;
       int64_t mm = m0 + c, nn = n0 + c;
-      As[kr][c] = (r < r1 && mm < d_in) ? Num<T>::to_f(xg[r * d_in + mm]) : 0.f;
-      Bs[kr][c] = (r < r1 && nn < d_out) ? Num<T>::to_f(yg[r * d_out + nn]) : 0.f;
+      // scattered operands: grouped position r reads row order[r] / fan_out
+      const int64_t ra = (r < r1 && !ga) ? order[r] / fa : r;
+      const int64_t rb = (r < r1 && !gb) ? order[r] / fb : r;
+      As[kr][c] = (r < r1 && mm < d_in) ? Num<T>::to_f(xg[ra * d_in + mm]) : 0.f;
+      Bs[kr][c] = (r < r1 && nn < d_out) ? Num<T>::to_f(yg[rb * d_out + nn]) : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -247,6 +252,22 @@ int simt_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E
     simt_xty_kernel<float><<<grid, S_THREADS, 0, st>>>((const float *)xg, (const float *)yg, offsets, d_in, d_out, (float *)dw);
   }
   return check_launch("simt_group_xty");
+}
+
+int simt_group_xty_scattered(const void *x, int fa, int ga, const void *y, int fb, int gb, const int32_t *order,
+                             const int32_t *offsets, int E, int64_t d_in, int64_t d_out, int dtype, void *dw,
+                             cudaStream_t st) {
+  if (d_in == 0 || d_out == 0) return SMOE_OK;
+  dim3 grid((unsigned)((d_out + SB_N - 1) / SB_N), (unsigned)((d_in + SB_M - 1) / SB_M), (unsigned)E);
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    simt_xty_kernel<T><<<grid, S_THREADS, 0, st>>>((const T *)x, (const T *)y, offsets, d_in, d_out, (T *)dw, order,
+                                                   fa, ga, fb, gb);
+  } else {
+    simt_xty_kernel<float><<<grid, S_THREADS, 0, st>>>((const float *)x, (const float *)y, offsets, d_in, d_out,
+                                                       (float *)dw, order, fa, ga, fb, gb);
+  }
+  return check_launch("simt_group_xty_scattered");
 }
 
 // y = round(y_accum) (bf16), or a no-op when y aliases the fp32 accumulator.

@@ -57,27 +57,34 @@ constexpr int TG_ROWS = 0;
 constexpr int G_RPT = (128 - TG_ROWS) / G_RSTEP;  // rows per cp.async gather thread per k-block
 constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
 constexpr int STG_BYTES = 32 * 128;        // per-epilogue-warp staging tile: 32 rows x 64 bf16
-__host__ __device__ constexpr int kernel_threads(int am) {
-  return 64 + 32 * EPI_WARPS + (am == A_GATHER ? 32 * GATHER_WARPS : 0);
+__host__ __device__ constexpr bool has_gather(int am, int bm) {
+  return am == A_GATHER || am == A_MN_G || bm == B_ROWS_MN_G;
+}
+__host__ __device__ constexpr int kernel_threads(int am, int bm) {
+  return 64 + 32 * EPI_WARPS + (has_gather(am, bm) ? 32 * GATHER_WARPS : 0);
 }
 
 template <int AM, int BMODE, bool GK, bool STAGED>
-__global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 1)
+__global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__(2, 1, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_c2, Params p) {
-  constexpr int THREADS = kernel_threads(AM);
+  constexpr int THREADS = kernel_threads(AM, BMODE);
   constexpr int STAGES = ring_stages(STAGED);
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
   // critical producer and MMA warps take the highest ids and never queue behind
   // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
-  constexpr int WP = EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0);
+  constexpr bool GATHER = has_gather(AM, BMODE);
+  // grouped-K with gathered operand(s): the cp.async warps fill them, TMA the rest
+  constexpr bool KGATHER = GK && GATHER;
+  constexpr bool GA = (AM == A_MN_G), GB = (BMODE == B_ROWS_MN_G);
+  constexpr int WP = EPI_WARPS + (GATHER ? GATHER_WARPS : 0);
   constexpr int WM = WP + 1;
   // cp.async data cannot signal the leader's barrier: gather mode relays it
-  constexpr bool RELAY = (AM == A_GATHER);
+  constexpr bool RELAY = GATHER;
   // Warps that read every tile id from the ring: both CTAs' epilogue (and
   // gather) warps, the leader's MMA warp, the peer's producer, and the peer's
   // relay / bin-tail fixer warp.
-  constexpr int RING_READERS = 2 * (EPI_WARPS + (AM == A_GATHER ? GATHER_WARPS : 0)) + 2 + ((RELAY || GK) ? 1 : 0);
+  constexpr int RING_READERS = 2 * (EPI_WARPS + (GATHER ? GATHER_WARPS : 0)) + 2 + ((RELAY || GK) ? 1 : 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&lfull_bar[s]), AM == A_GATHER ? 1 + 32 * GATHER_WARPS : 1);
+      mbar_init(smem_u32(&lfull_bar[s]), GATHER ? 1 + 32 * GATHER_WARPS : 1);
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -213,7 +220,19 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         if (elect_one_sync()) {
           const uint32_t sb = sa + A_BYTES;
-          if (RELAY) {
+          if (KGATHER) {
+            // this CTA's TMA bytes (non-gathered operand) are counted locally;
+            // the leader also expects the peer's 16-byte relay signal
+            mbar_expect_tx(fb, (GA ? 0 : A_BYTES) + (GB ? 0 : B_BYTES) + (leader ? 16 : 0));
+            if (!GB) {
+              tma_load_2d(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
+              tma_load_2d(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
+            }
+            if (!GA) {
+              tma_load_2d(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
+              tma_load_2d(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+            }
+          } else if (RELAY) {
             // gather mode: this CTA's bytes are counted locally; the leader also
             // expects the peer's 16-byte relay signal on the same barrier
             mbar_expect_tx(fb, B_BYTES + TG_ROWS * 128 + (leader ? 16 : 0));
@@ -268,7 +287,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
   } else if (warp == WM) {
     if (leader) {
       // ===================== MMA issuer (leader CTA) =====================
-      constexpr uint32_t a_mn = (AM == A_MN) ? 1u : 0u;
+      constexpr uint32_t a_mn = (AM == A_MN || GA) ? 1u : 0u;
       constexpr uint32_t b_mn = (BMODE == B_W_K) ? 0u : 1u;
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) |
                                  ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
-              if (valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
+              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
             }
           }
           if (RELAY) fence_proxy_async_smem();
@@ -313,7 +332,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
             for (int k = 0; k < BK / 16; ++k) {
               if (GK && k >= nk) break;
               uint64_t ad, bd;
-              if (AM == A_MN) ad = sdesc(sa + k * 2048, 8192, 1024);
+              if (AM == A_MN || GA) ad = sdesc(sa + k * 2048, 8192, 1024);
               else ad = sdesc(sa + k * 32, 16, 1024);
               if (BMODE == B_W_K) bd = sdesc(sb + k * 32, 16, 1024);
               else bd = sdesc(sb + k * 2048, 8192, 1024);
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         printf("tc2 timing cluster %d: total %lld cyc, wait tempty %lld (%.1f%%), wait lfull %lld (%.1f%%)\n",
                (int)cluster_id, clock64() - c_start, c_tempty, 100.0 * c_tempty / (clock64() - c_start), c_lfull,
                100.0 * c_lfull / (clock64() - c_start));
-    } else if (GK) {
+    } else if (GK && !RELAY) {
       // ===================== tail fixer (peer CTA, grouped-K) =====================
       // For each tile's bin-tail stage: wait for this CTA's own bytes, zero the
       // A rows past the bin, then signal the leader's lfull (16-byte DSMEM bulk
@@ -367,6 +386,13 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          if (KGATHER && !(GA && GB)) {
+            // grouped-K bin tail: the TMA operand's rows past the bin belong to
+            // the next expert; zero them up to the K16 step the leader issues
+            const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+            const int upto = 16 * ((valid + 15) / 16);
+            if (valid < BK && valid < upto) zero_k_rows(tiles_smem + stage * STAGE_BYTES, 4, valid, upto, lane);
+          }
           fence_proxy_async_smem();
           __syncwarp();
           // Signal the leader through the async proxy: a 16-byte DSMEM bulk copy
@@ -598,6 +624,82 @@ __global__ void __launch_bounds__(kernel_threads(AM), 1) __cluster_dims__(2, 1, 
         }
       }
     }
+  } else if (KGATHER) {
+    // ===================== cp.async gather of grouped-K operand rows =====================
+    // Per k-block each gathered operand is 64 K rows (bin slots) x this CTA's
+    // 128 M (or N) columns = two 64-row x 128-B boxes, 128-B swizzled.  Thread
+    // (rsub, chunk) copies 16-byte chunk `chunk` of rows rsub + 8 q; rows past
+    // the bin and columns past the matrix are zero-filled (src-size 0).
+    const int g = threadIdx.x - 32 * EPI_WARPS;
+    const int chunk = g & 15;
+    const int rsub = g >> 4;
+    const int box = chunk >> 3, cq = chunk & 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+      const int64_t t = next_tile(it);
+      if (t < 0) break;
+      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const int64_t acol = tl.m0 + HM * rank + chunk * 8;
+      const int64_t bcol = tl.n0 + HN * rank + chunk * 8;
+      const bool a_ok = acol < p.M, b_ok = bcol < p.N;
+      // Source rows run IDX_PF k-blocks ahead.  Per k-block each warp needs the
+      // 16 bin rows 2w + b + 8q (b = lane >> 4, q = 0..7).  Lane b + 2q turns
+      // row q's slot into the A source row's offset in 16-byte chunks
+      // ((slot / fan_out) * M / 8; bit 31 set = past the bin), lane
+      // 16 + b + 2q the B offset, and the warp shares them by shuffles: the
+      // copy loop does one shuffle, one address and one cp.async per row.
+      const int wl = g >> 5;
+      const int64_t prow = 2 * wl + (lane & 1) + 8 * ((lane >> 1) & 7);
+      const uint32_t fdiv = (uint32_t)(lane < 16 ? p.fan_out : p.fan_out_b);
+      const uint32_t rchunks = (uint32_t)((lane < 16 ? p.M : p.N) >> 3);
+      // raw slot ids are loaded IDX_PF k-blocks ahead and converted only when used
+      const int32_t *optr = p.order + tl.k0 + prow;
+      const int64_t rows_left = tl.k_len - prow;  // row kb*BK + prow exists iff kb*BK < rows_left
+      auto ld_slot = [&](int kb) -> int32_t {
+        return (int64_t)kb * BK < rows_left ? __ldg(optr + (int64_t)kb * BK) : -1;
+      };
+      constexpr int IDX_PF = 4;
+      int32_t pf[IDX_PF];
+#pragma unroll
+      for (int j = 0; j < IDX_PF; ++j) pf[j] = ld_slot(j);
+      const uint4 *xa = reinterpret_cast<const uint4 *>(p.x + (a_ok ? acol : 0));
+      const uint4 *yb = reinterpret_cast<const uint4 *>(p.y + (b_ok ? bcol : 0));
+      const uint32_t asz = a_ok ? 16u : 0u, bsz = b_ok ? 16u : 0u;
+      uint32_t doff[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int r = rsub + 8 * q;
+        doff[q] = box * 8192 + r * 128 + ((cq ^ (r & 7)) << 4);
+      }
+      // unrolled by IDX_PF so each prefetch register is consumed in place (a
+      // register rotation would wait on the loads still in flight)
+      for (int kb0 = 0; kb0 < tl.nkb; kb0 += IDX_PF) {
+#pragma unroll
+        for (int j = 0; j < IDX_PF; ++j) {
+          const int kb = kb0 + j;
+          if (kb >= tl.nkb) break;
+          const uint32_t mine = pf[j] >= 0 ? ((uint32_t)pf[j] / fdiv) * rchunks : 0x80000000u;
+          pf[j] = ld_slot(kb + IDX_PF);
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (GA) {
+              const uint32_t o = __shfl_sync(0xffffffffu, mine, (lane >> 4) + 2 * q);
+              cp_async16(sa + doff[q], xa + (o & 0x7fffffffu), asz & ~(uint32_t)((int32_t)o >> 31));
+            }
+            if (GB) {
+              const uint32_t o = __shfl_sync(0xffffffffu, mine, 16 + (lane >> 4) + 2 * q);
+              cp_async16(sb + doff[q], yb + (o & 0x7fffffffu), bsz & ~(uint32_t)((int32_t)o >> 31));
+            }
+          }
+          cp_async_arrive_noinc(smem_u32(&lfull_bar[stage]));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
   } else if (AM == A_GATHER) {
     // ===================== cp.async gather of this CTA's 128 A rows =====================
     const int g = threadIdx.x - 32 * EPI_WARPS;
@@ -721,7 +823,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   Params q = p;
   q.tile_ctr = tile_counter(st);
   if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
-  kern<<<2 * clusters, kernel_threads(AM), smem, st>>>(ta, tb, tc, tc2, q);
+  kern<<<2 * clusters, kernel_threads(AM, BMODE), smem, st>>>(ta, tb, tc, tc2, q);
   return check_launch("tc2_gemm");
 }
 
@@ -875,6 +977,50 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
   if (staged_for(false, true, INT64_MAX)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);
   return launch<A_MN, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
+}
+
+// group_xty over scattered operands (parallel_linear.py:224-234 without the
+// grouped copies): operand rows are gathered by slot (order[i] / fan_out) when
+// the operand is scattered, read by TMA when it is already grouped.
+int group_xty_scattered(const void *x, int64_t x_rows, int fa, int ga, const void *y, int64_t y_rows, int fb, int gb,
+                        const int32_t *order, const int32_t *offsets, int E, int64_t n, int64_t d_in, int64_t d_out,
+                        void *dw, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[2] = {(uint64_t)d_in, (uint64_t)(x_rows > 0 ? x_rows : 1)};
+    uint64_t strides[1] = {(uint64_t)d_in * 2};
+    uint32_t box[2] = {64, 64};
+    if (!encode_map(&ta, x, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(X) failed");
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)d_out, (uint64_t)(y_rows > 0 ? y_rows : 1)};
+    uint64_t strides[1] = {(uint64_t)d_out * 2};
+    uint32_t box[2] = {64, 64};
+    if (!encode_map(&tb, y, 2, dims, strides, box)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(Y) failed");
+  }
+  Params p{};
+  p.E = E;
+  p.M = d_in;
+  p.N = d_out;
+  p.K = 0;
+  p.order = order;
+  p.offsets = offsets;
+  p.fan_out = fa;
+  p.fan_out_b = fb;
+  p.x = (const __nv_bfloat16 *)x;
+  p.y = (const __nv_bfloat16 *)y;
+  p.grouped_out = 1;
+  p.epi = SMOE_EPI_NONE;
+  p.out = (__nv_bfloat16 *)dw;
+  p.group_m = group_m_k_setting();
+  p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
+  const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
+  CUtensorMap tc;
+  if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
+  if (ga && gb) return launch<A_MN, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
+  if (gb) return launch<A_MN_G, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
+  if (ga) return launch<A_MN, B_ROWS_MN_G, true, false>(ta, tb, tc, tc, p, max_tiles, st);
+  return launch<A_MN_G, B_ROWS_MN_G, true, false>(ta, tb, tc, tc, p, max_tiles, st);
 }
 
 }  // namespace tc2

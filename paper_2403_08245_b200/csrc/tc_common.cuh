@@ -9,8 +9,10 @@
 namespace smoe {
 namespace tc {
 
-enum AMode { A_ROWS = 0, A_GATHER = 1, A_MN = 2 };
-enum BMode { B_W_MN = 0, B_W_K = 1, B_ROWS_MN = 2 };
+// A_MN_G / B_ROWS_MN_G: grouped-K operands gathered row by row from a scattered
+// tensor (slot i of the bin reads row order[i] / fan_out) by the cp.async warps.
+enum AMode { A_ROWS = 0, A_GATHER = 1, A_MN = 2, A_MN_G = 3 };
+enum BMode { B_W_MN = 0, B_W_K = 1, B_ROWS_MN = 2, B_ROWS_MN_G = 3 };
 // Internal epilogue (smoe_scatter_combine, not a public SMOE_EPI_* value): each
 // accumulator row is scaled by its slot's combine weight and added into the
 // fp32 token row yacc[order[i] / combine_cols] (vector reductions in L2).
@@ -37,6 +39,8 @@ struct Params {
   const float *pw;         // EPI_COMBINE: combine weight per scattered slot
   float *yacc;             // EPI_COMBINE: fp32 [n / combine_cols, N] accumulator
   int combine_cols;        // EPI_COMBINE: slots per output row
+  const __nv_bfloat16 *y;  // B_ROWS_MN_G: the scattered B rows [y_rows, N]
+  int fan_out_b;           // B_ROWS_MN_G: slots per B row
 };
 
 // ---- PTX wrappers ------------------------------------------------------------

@@ -404,6 +404,8 @@ int scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, 
 int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
 int scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
                     int64_t, int, int, const float *, int, float *, cudaStream_t);
+int group_xty_scattered(const void *, int64_t, int, int, const void *, int64_t, int, int, const int32_t *,
+                        const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -489,6 +491,25 @@ int tc_scatter_combine(const void *x, int64_t x_rows, const void *w, int E, int6
                               "16-byte aligned buffers");
   return tc2::scatter_combine(x, x_rows, w, E, d_in, d_out, order, offsets, n, fan_out, gin, p_flat, combine_cols,
                               yacc, st);
+}
+
+// gathered rows are addressed by 31-bit offsets in 16-byte chunks
+static bool xty_offsets_fit(int64_t rows, int64_t cols) { return rows * (cols / 8) < (1ll << 31); }
+
+// group_xty with scattered (gathered) operands: CTA-pair kernels only.
+bool tc_supports_xty_scattered(int E, int64_t x_rows, int64_t d_in, int64_t y_rows, int64_t d_out, const void *x,
+                               const void *y, const void *dw) {
+  return tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && d_in % 8 == 0 && d_out % 8 == 0 && al16(x) &&
+         al16(y) && al16(dw) && xty_offsets_fit(x_rows, d_in) && xty_offsets_fit(y_rows, d_out);
+}
+
+int tc_group_xty_scattered(const void *x, int64_t x_rows, int fa, int ga, const void *y, int64_t y_rows, int fb,
+                           int gb, const int32_t *order, const int32_t *offsets, int E, int64_t n, int64_t d_in,
+                           int64_t d_out, void *dw, cudaStream_t st) {
+  if (!tc_supports_xty_scattered(E, x_rows, d_in, y_rows, d_out, x, y, dw))
+    return fail(SMOE_ENOTSUP, "tcgen05 group_xty over scattered operands needs the CTA-pair engine, d_in, d_out "
+                              "multiples of 8 and 16-byte aligned buffers");
+  return tc2::group_xty_scattered(x, x_rows, fa, ga, y, y_rows, fb, gb, order, offsets, E, n, d_in, d_out, dw, st);
 }
 
 int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in,

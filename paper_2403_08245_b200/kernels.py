@@ -348,6 +348,52 @@ def group_xty(
     return out
 
 
+def group_xty_scattered(
+    x: torch.Tensor,
+    y: torch.Tensor,
+    order: GroupedOrder,
+    *,
+    x_fan_out: int = 1,
+    y_fan_out: int = 1,
+    x_grouped: bool = False,
+    y_grouped: bool = False,
+    out: torch.Tensor | None = None,
+    engine: str | None = None,
+) -> torch.Tensor:
+    """group_xty(group(x, fan_out=x_fan_out), group(y, fan_out=y_fan_out)) without the grouped copies.
+
+    Row i of a bin reads x[order.o[i] // x_fan_out] (x[i] when x_grouped), likewise y:
+    the reference's parallel_linear.py:224-234 (group + group_xty) fused into the
+    GEMM's operand loads.
+    """
+    num_slots = order.num_slots
+    for name, a, f, grouped in (("x", x, x_fan_out, x_grouped), ("y", y, y_fan_out, y_grouped)):
+        if f < 1:
+            raise ValueError(f"{name}_fan_out must be >= 1, got {f}")
+        want = num_slots if grouped else num_slots // f
+        if a.shape[0] != want or (not grouped and a.shape[0] * f != num_slots):
+            raise ValueError(f"{name} rows ({a.shape[0]}) do not cover the {num_slots} slots "
+                             f"({'grouped' if grouped else f'fan_out {f}'})")
+    if x.dtype != y.dtype:
+        raise ValueError(f"group_xty operands must share a dtype, got {x.dtype} and {y.dtype}")
+    x, y = _cuda(x, "x"), _cuda(y, "y")
+    d_in, d_out = x.shape[1], y.shape[1]
+    e = order.num_experts
+    if out is None:
+        out = torch.empty((e, d_in, d_out), dtype=x.dtype, device=x.device)
+    else:
+        require_dims(tuple(out.shape) == (e, d_in, d_out), "dw buffer", tuple(out.shape), (e, d_in, d_out))
+    t0 = _lt.begin()
+    st = _lib.load().smoe_group_xty_scattered(
+        x.data_ptr(), x.shape[0], x_fan_out, int(x_grouped), y.data_ptr(), y.shape[0], y_fan_out, int(y_grouped),
+        order.o.data_ptr(), order.bin_offsets.data_ptr(), e, num_slots, d_in, d_out, _dtype_id(x),
+        out.data_ptr(), _engine_id(engine), _stream(x))
+    _lt.end("group_xty " + ("G" if x_grouped else "S") + ("G" if y_grouped else "S"), t0)
+    _lib.check(st, "group_xty_scattered")
+    _credit(order, d_in, d_out)
+    return out
+
+
 # ---- row kernels used by parallel_linear (not in the reference's kernels.py) ----
 
 def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

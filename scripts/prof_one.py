@@ -52,6 +52,8 @@ for _ in range(3):
         sm.group_xty(h, xg, order_al)
     elif which == "cublas":  # dense library GEMM with the same FLOPs (n x d @ d x d_e)
         torch.matmul(xg, w[0])
+    elif which == "xtysg":  # dW1 with X gathered by slot (no grouped copy)
+        sm.kernels.group_xty_scattered(x, h, order, x_fan_out=k, y_grouped=True)
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()

@@ -217,3 +217,40 @@ def test_inference_mlp_uses_tcgen05_combine():
     assert any(lab.startswith("scatter_combine") for lab in labels), labels
     y_tr, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=True)
     assert rel_err(y_inf, np_of(y_tr)) <= 1e-2
+
+
+@pytest.mark.parametrize("engine", ["auto", "simt"])
+@pytest.mark.parametrize("flavor", ["gate", "all_to_one", "skip_one"])
+@pytest.mark.parametrize("grouped", [(False, True), (True, False), (False, False)])
+def test_group_xty_scattered_matches_group_then_xty(engine, flavor, grouped):
+    """Gathered weight-gradient operands == the reference's group() copies + group_xty
+    (bit-identical on the tensor cores: same rows land in the same smem slots)."""
+    xg_flag, yg_flag = grouped
+    rng = np.random.default_rng(hash(("xtys", flavor, grouped)) % 2**32)
+    dt = torch.bfloat16 if engine == "auto" else torch.float32
+    for tokens, k, e, d_in, d_out in [(300, 2, 6, 256, 512), (1000, 3, 8, 136, 264), (77, 1, 5, 64, 192),
+                                      (4096, 2, 8, 512, 256)]:
+        idx, _, _, _ = _problem(rng, tokens, k, e, 8, 8, sm.SCATTERED_TO_GROUPED, False, flavor)
+        n = tokens * k
+        fx, fy = (1 if xg_flag else k), (1 if yg_flag else 1)
+        x = bf16_round(rng.uniform(-1, 1, (n if xg_flag else n // fx, d_in)).astype(np.float32))
+        y = bf16_round(rng.uniform(-1, 1, (n if yg_flag else n // fy, d_out)).astype(np.float32))
+        order = order_of(idx, e)
+        xt, yt = t(x, dt), t(y, dt)
+        got = sm.kernels.group_xty_scattered(xt, yt, order, x_fan_out=fx, y_fan_out=fy, x_grouped=xg_flag,
+                                             y_grouped=yg_flag, engine=engine)
+        xb = xt if xg_flag else sm.group(xt, order, fan_out=fx)
+        yb = yt if yg_flag else sm.group(yt, order, fan_out=fy)
+        want = sm.group_xty(xb, yb, order, engine=engine)
+        if engine == "auto":
+            assert torch.equal(got, want), (tokens, k, e)
+        else:
+            o, off = orc.compute_grouped_order(idx, e)
+            xo = x if xg_flag else x[o // fx]
+            yo = y if yg_flag else y[o // fy]
+            ref = orc.group_xty(xo, yo, off)
+            # fp32 sums of up to ~3000 products of magnitude <= 1 vs f64
+            np.testing.assert_allclose(np_of(got), ref, rtol=FP32_RTOL, atol=1e-4)
+            assert rel_err(got, ref) <= 1e-5
+        if flavor == "skip_one":
+            assert float(got[e - 1].abs().max()) == 0.0
