@@ -60,8 +60,14 @@ constexpr int STG_BYTES = 32 * 128;        // per-epilogue-warp staging tile: 32
 __host__ __device__ constexpr bool has_gather(int am, int bm) {
   return am == A_GATHER || am == A_MN_G || bm == B_ROWS_MN_G;
 }
+// Copy warps of the grouped-K gather (rows change every k-block).  8 warps
+// measured slower than 4 (C1 dW1 7.3 vs 7.0 ms in-step; profiles/r1_gather_ab.txt).
+constexpr int KG_WARPS = 4;
+__host__ __device__ constexpr int gather_warps(int am, int bm) {
+  return am == A_GATHER ? GATHER_WARPS : (has_gather(am, bm) ? KG_WARPS : 0);
+}
 __host__ __device__ constexpr int kernel_threads(int am, int bm) {
-  return 64 + 32 * EPI_WARPS + (has_gather(am, bm) ? 32 * GATHER_WARPS : 0);
+  return 64 + 32 * EPI_WARPS + 32 * gather_warps(am, bm);
 }
 
 template <int AM, int BMODE, bool GK, bool STAGED>
@@ -77,14 +83,15 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   // grouped-K with gathered operand(s): the cp.async warps fill them, TMA the rest
   constexpr bool KGATHER = GK && GATHER;
   constexpr bool GA = (AM == A_MN_G), GB = (BMODE == B_ROWS_MN_G);
-  constexpr int WP = EPI_WARPS + (GATHER ? GATHER_WARPS : 0);
+  constexpr int GW = gather_warps(AM, BMODE);
+  constexpr int WP = EPI_WARPS + GW;
   constexpr int WM = WP + 1;
   // cp.async data cannot signal the leader's barrier: gather mode relays it
   constexpr bool RELAY = GATHER;
   // Warps that read every tile id from the ring: both CTAs' epilogue (and
   // gather) warps, the leader's MMA warp, the peer's producer, and the peer's
   // relay / bin-tail fixer warp.
-  constexpr int RING_READERS = 2 * (EPI_WARPS + (GATHER ? GATHER_WARPS : 0)) + 2 + ((RELAY || GK) ? 1 : 0);
+  constexpr int RING_READERS = 2 * (EPI_WARPS + GW) + 2 + ((RELAY || GK) ? 1 : 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
@@ -117,7 +124,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&lfull_bar[s]), GATHER ? 1 + 32 * GATHER_WARPS : 1);
+      mbar_init(smem_u32(&lfull_bar[s]), GATHER ? 1 + 32 * GW : 1);
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -628,8 +635,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     // ===================== cp.async gather of grouped-K operand rows =====================
     // Per k-block each gathered operand is 64 K rows (bin slots) x this CTA's
     // 128 M (or N) columns = two 64-row x 128-B boxes, 128-B swizzled.  Thread
-    // (rsub, chunk) copies 16-byte chunk `chunk` of rows rsub + 8 q; rows past
-    // the bin and columns past the matrix are zero-filled (src-size 0).
+    // (rsub, chunk) copies 16-byte chunk `chunk` of rows rsub + RSTR q; rows
+    // past the bin and columns past the matrix are zero-filled (src-size 0).
+    constexpr int RPT = GW > 0 ? 32 / GW : 1;  // rows per thread per k-block
+    constexpr int RSTR = 2 * GW;       // row stride between a thread's rows
     const int g = threadIdx.x - 32 * EPI_WARPS;
     const int chunk = g & 15;
     const int rsub = g >> 4;
@@ -644,13 +653,13 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       const int64_t bcol = tl.n0 + HN * rank + chunk * 8;
       const bool a_ok = acol < p.M, b_ok = bcol < p.N;
       // Source rows run IDX_PF k-blocks ahead.  Per k-block each warp needs the
-      // 16 bin rows 2w + b + 8q (b = lane >> 4, q = 0..7).  Lane b + 2q turns
+      // 2 RPT bin rows 2w + b + RSTR q (b = lane >> 4).  Lane b + 2q turns
       // row q's slot into the A source row's offset in 16-byte chunks
       // ((slot / fan_out) * M / 8; bit 31 set = past the bin), lane
       // 16 + b + 2q the B offset, and the warp shares them by shuffles: the
       // copy loop does one shuffle, one address and one cp.async per row.
       const int wl = g >> 5;
-      const int64_t prow = 2 * wl + (lane & 1) + 8 * ((lane >> 1) & 7);
+      const int64_t prow = 2 * wl + (lane & 1) + RSTR * ((lane >> 1) & (RPT - 1));
       const uint32_t fdiv = (uint32_t)(lane < 16 ? p.fan_out : p.fan_out_b);
       const uint32_t rchunks = (uint32_t)((lane < 16 ? p.M : p.N) >> 3);
       // raw slot ids are loaded IDX_PF k-blocks ahead and converted only when used
@@ -666,10 +675,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       const uint4 *xa = reinterpret_cast<const uint4 *>(p.x + (a_ok ? acol : 0));
       const uint4 *yb = reinterpret_cast<const uint4 *>(p.y + (b_ok ? bcol : 0));
       const uint32_t asz = a_ok ? 16u : 0u, bsz = b_ok ? 16u : 0u;
-      uint32_t doff[8];
+      uint32_t doff[RPT];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int r = rsub + 8 * q;
+      for (int q = 0; q < RPT; ++q) {
+        const int r = rsub + RSTR * q;
         doff[q] = box * 8192 + r * 128 + ((cq ^ (r & 7)) << 4);
       }
       // unrolled by IDX_PF so each prefetch register is consumed in place (a
@@ -685,7 +694,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < RPT; ++q) {
             if (GA) {
               const uint32_t o = __shfl_sync(0xffffffffu, mine, (lane >> 4) + 2 * q);
               cp_async16(sa + doff[q], xa + (o & 0x7fffffffu), asz & ~(uint32_t)((int32_t)o >> 31));

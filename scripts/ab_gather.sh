@@ -3,9 +3,9 @@
 # on C1, C2 (bench.py) and C3 (momha_bench.py); twice each, interleaved.
 for rep in 1 2; do
   for g in 0 1; do
-    SMOE_GATHER_OPERANDS=$g timeout 300 python bench.py --config C1 --no-cpu-baseline > gpurun_out/ab_c1_g${g}_$rep.log 2>&1
-    SMOE_GATHER_OPERANDS=$g timeout 300 python bench.py --config C2 --no-cpu-baseline > gpurun_out/ab_c2_g${g}_$rep.log 2>&1
-    SMOE_GATHER_OPERANDS=$g timeout 300 python scripts/momha_bench.py > gpurun_out/ab_c3_g${g}_$rep.log 2>&1
+    SMOE_GATHER_MAX_DOUT=${MAXD:-1024} SMOE_GATHER_OPERANDS=$g timeout 300 python bench.py --config C1 --no-cpu-baseline > gpurun_out/ab_c1_g${g}_$rep.log 2>&1
+    SMOE_GATHER_MAX_DOUT=${MAXD:-1024} SMOE_GATHER_OPERANDS=$g timeout 300 python bench.py --config C2 --no-cpu-baseline > gpurun_out/ab_c2_g${g}_$rep.log 2>&1
+    SMOE_GATHER_MAX_DOUT=${MAXD:-1024} SMOE_GATHER_OPERANDS=$g timeout 300 python scripts/momha_bench.py > gpurun_out/ab_c3_g${g}_$rep.log 2>&1
   done
 done
 python - <<'PY'
