@@ -202,14 +202,18 @@ def run_ours(args, rank, world, local_rank):
         from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
         ep = ExpertParallelSmoeMlp(w1, w2, E)
 
-        def step(xx, dyy, rt):
+        def step(xx, dyy, rt, dy_ready=None):
             y, ctx = ep.forward(xx, rt)
+            if dy_ready is not None:
+                dy_ready()
             grads = ep.backward(ctx, dyy)
             return y, grads
     else:
-        def step(xx, dyy, rt):
+        def step(xx, dyy, rt, dy_ready=None):
             order = sm.compute_grouped_order(rt)
             y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
+            if dy_ready is not None:   # e2e: dY's H2D copy overlaps the forward
+                dy_ready()
             grads = sm.smoe_mlp_backward(ctx, dyy)
             return y, grads
 
@@ -267,18 +271,20 @@ def run_ours(args, rank, world, local_rank):
     cs = torch.cuda.Stream(device=dev)
     dbufs = [dict(x=torch.empty_like(x), dy=torch.empty_like(dy), ids=torch.empty_like(routing.expert_idx),
                   p=torch.empty_like(routing.p)) for _ in range(2)]
-    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]      # forward inputs (ids, p, X) landed
+    ev_dy = [torch.cuda.Event() for _ in range(2)]      # dY landed (needed only by the backward)
     ev_done = [torch.cuda.Event() for _ in range(2)]
 
     def prefetch_inputs(slot):
         b = dbufs[slot]
         with torch.cuda.stream(cs):
             cs.wait_event(ev_done[slot])             # the step that last used this slot has finished
-            b["x"].copy_(hx, non_blocking=True)
-            b["dy"].copy_(hdy, non_blocking=True)
             b["ids"].copy_(hidx, non_blocking=True)
             b["p"].copy_(hp, non_blocking=True)
+            b["x"].copy_(hx, non_blocking=True)
             ev_in[slot].record(cs)
+            b["dy"].copy_(hdy, non_blocking=True)
+            ev_dy[slot].record(cs)
 
     def e2e_run(n_steps):
         for s_ in range(2):
@@ -292,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
             b = dbufs[slot]
             rt = sm.RoutingResult(expert_idx=b["ids"], p=b["p"], gate_full=routing.gate_full, renormalized=True,
                                   validate=False)
-            _, grads = step(b["x"], b["dy"], rt)
+            _, grads = step(b["x"], b["dy"], rt, dy_ready=lambda: st.wait_event(ev_dy[slot]))
             ev_done[slot].record(st)
             with torch.cuda.stream(cs):
                 cs.wait_event(ev_done[slot])
