@@ -197,10 +197,16 @@ def run_ours(args, rank, world, local_rank):
     routing = sm.topk_select(sm.gate_forward(x.float(), wg), k)
     torch.cuda.synchronize()
 
-    if world > 1:
+    ep_mode = args.ep if args.ep != "auto" else ("peer" if world > 1 else "none")
+    if ep_mode != "none":
         # expert parallelism: this rank owns experts [rank*E/G, (rank+1)*E/G)
-        from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
-        ep = ExpertParallelSmoeMlp(w1, w2, E)
+        if ep_mode == "peer":
+            # rows stored straight into the owner's buffers over peer memory (ep_peer.py)
+            from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
+            ep = PeerExpertParallelSmoeMlp(w1, w2, E, k, max_tokens=T)
+        else:
+            from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
+            ep = ExpertParallelSmoeMlp(w1, w2, E)
 
         def step(xx, dyy, rt, dy_ready=None):
             y, ctx = ep.forward(xx, rt)
@@ -329,7 +335,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- roofline: dominant kernel (layer-1 forward grouped GEMM) ----
     # achieved = its algorithmic FLOPs / its mean launch duration inside the
     # timed steps (events on its stream); it is also timed alone for reference.
-    if world > 1:
+    if ep_mode != "none":
         # this rank's local experts only (the EP shard)
         kk = min(k, e_local)
         rt_local = sm.topk_select(torch.softmax(torch.randn(T, e_local, device=dev, generator=g), 1), kk)
@@ -389,7 +395,9 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, softmax top-k routing)",
             "config": {"workload": desc, "global_batch": T * world, "seq_len": None,
-                       "parallelism": f"ep{world} (experts sharded, NCCL all-to-all-v dispatch/combine)" if world > 1
+                       "parallelism": (f"ep{world} (experts sharded; " + ("rows stored into the owners' buffers over "
+                                       "peer memory, ep_peer.py)" if ep_mode == "peer" else
+                                       "NCCL all-to-all-v dispatch/combine, ep.py)")) if ep_mode != "none"
                        else "single GPU",
                        "l2": "inputs larger than L2 (W1+W2 1.9 GB, H 1.9 GB); no flush",
                        "engine": sm.get_engine(), "timed": "flatten_and_sort + smoe_mlp_forward + smoe_mlp_backward"},
@@ -418,6 +426,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default=None)
+    ap.add_argument("--ep", default="auto", choices=["auto", "peer", "nccl", "none"],
+                    help="expert-parallel exchange (auto: peer memory when N>1, none at N=1; "
+                         "peer/nccl at N=1 time the EP path on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -432,16 +443,21 @@ def main():
     if args.engine:
         import paper_2403_08245_b200 as sm
         sm.set_engine(args.engine)
-    if world > 1:
+    if world > 1 or args.ep in ("peer", "nccl"):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
             dist.destroy_process_group()
 
 

@@ -182,6 +182,43 @@ int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t n
                          const float *p_flat, int32_t combine_cols, int32_t grouped_in,
                          int32_t dtype, float *y_accum, void *y, int32_t engine, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Expert parallelism over peer memory (the
+ * reference has no multi-device code).  Buffers of other ranks are
+ * CUDA IPC mappings (NVLink P2P across GPUs; plain device memory between
+ * processes sharing one GPU).  `peer_*` arguments are DEVICE arrays of
+ * world_size uint64 base addresses, one per rank (this rank's own included).
+ */
+size_t smoe_ipc_handle_bytes(void);
+/* handle of the allocation holding dev_ptr, and dev_ptr's byte offset in it */
+int smoe_ipc_get_handle(const void *dev_ptr, void *handle_out /* host, smoe_ipc_handle_bytes() */,
+                        int64_t *offset_out /* host */);
+/* map a peer allocation; returns its base (add the peer's offset) */
+int smoe_ipc_open(const void *handle /* host */, void **dev_ptr_out /* host */);
+int smoe_ipc_close(void *dev_ptr /* the base smoe_ipc_open returned */);
+
+/* Dispatch: grouped row i of this rank (global expert e = sorted_expert[i],
+ * owner q = e / experts_per_rank) is stored at row dstart[e] + i - bin_offsets[e]
+ * of peer_rows[q]: x[order[i] / fan_out] (* weights[order[i]] if weights != NULL,
+ * the p-weighted group of parallel_linear.py:213).  With peer_slot/peer_src the
+ * row's slot id and this rank id are stored alongside (forward dispatch). */
+int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_t *order,
+                          const int32_t *sorted_expert, const int32_t *bin_offsets, int32_t fan_out,
+                          const float *weights, int64_t n, const int64_t *dstart, int32_t experts_per_rank,
+                          const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src,
+                          int32_t me, int32_t dtype, void *stream);
+/* Return: local row j goes to row recv_slot[j] of peer_out[recv_src[j]]. */
+int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv_slot, const int32_t *recv_src,
+                        const uint64_t *peer_out, int32_t dtype, void *stream);
+/* Copy `bytes` from src to every peer_dst[q] + offset_bytes. */
+int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,
+                void *stream);
+/* Signal every peer (system fence, then +1 on peer q's flags[slot * world + me]) /
+ * wait until flags[slot * world + s] >= target for every source s (err = 1 on timeout). */
+int smoe_ep_signal(const uint64_t *peer_flags, int32_t world, int32_t me, int32_t slot, void *stream);
+int smoe_ep_wait(const uint64_t *flags, int32_t world, int32_t slot, uint64_t target, int64_t timeout_ns,
+                 int32_t *err, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,16 @@ SIGNATURES = {
     "smoe_combine_grad_p": (_c.c_int, [_vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_fanout_reduce": (_c.c_int, [_vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_apply_activation": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_ipc_handle_bytes": (_sz, []),
+    "smoe_ipc_get_handle": (_c.c_int, [_vp, _vp, _c.POINTER(_c.c_int64)]),
+    "smoe_ipc_open": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p)]),
+    "smoe_ipc_close": (_c.c_int, [_vp]),
+    "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp,
+                                         _i32, _i32, _vp]),
+    "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_ep_put": (_c.c_int, [_vp, _i64, _vp, _i64, _i32, _vp]),
+    "smoe_ep_signal": (_c.c_int, [_vp, _i32, _i32, _i32, _vp]),
+    "smoe_ep_wait": (_c.c_int, [_vp, _i32, _i32, _c.c_uint64, _i64, _vp, _vp]),
     "smoe_group_xty_scattered": (_c.c_int, [_vp, _i64, _i32, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i64,
                                             _i64, _i64, _i32, _vp, _i32, _vp]),
     "smoe_scatter_combine": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,

@@ -1,0 +1,239 @@
+// Expert-parallel dispatch / return over peer memory (NVLink / NVSwitch P2P).
+//
+// SURVEY.md §8(e) and §8(f)-2.  Instead of packing rows into a send buffer and
+// calling an all-to-all, each rank stores its routed rows straight into the
+// owning rank's receive buffer — already at their final position in the
+// receiver's local grouped order (expert-major, then source rank, then source
+// order), so the receiver runs its grouped GEMMs on the rows as they landed
+// (TMA-fed, no group() copy) — and the expert outputs travel back the same way
+// into the source's slot-ordered buffer.  Peer buffers are CUDA IPC mappings
+// (smoe_ipc_*), so the same kernels run across GPUs (P2P over NVLink) and
+// across processes sharing one GPU (the single-GPU test rig).
+//
+// Completion: a signal kernel (system-scope fence, then one atomic increment
+// per peer on that peer's flag word for this source) and a wait kernel (spin
+// on the local flags until every source reached the expected epoch, with a
+// timeout that reports SMOE_ECUDA through an error word instead of hanging).
+#include <cuda.h>
+
+#include <cstring>
+
+#include "common.cuh"
+
+namespace smoe {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// grouped row i of this rank -> (destination rank, row in its receive buffer);
+// dstart[e] = first receive row of (this source, global expert e) at the owner.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) dispatch_kernel(const T *__restrict__ x, int64_t d,
+                                                            const int32_t *__restrict__ order,
+                                                            const int32_t *__restrict__ sorted_expert,
+                                                            const int32_t *__restrict__ bin_offsets, int fan_out,
+                                                            const float *__restrict__ weights, int64_t n,
+                                                            const int64_t *__restrict__ dstart, int e_per_rank,
+                                                            const uint64_t *__restrict__ peer_rows,
+                                                            const uint64_t *__restrict__ peer_slot,
+                                                            const uint64_t *__restrict__ peer_src, int me) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int32_t slot = order[i];
+  const int e = sorted_expert[i];
+  const int q = e / e_per_rank;
+  const int64_t j = dstart[e] + (i - bin_offsets[e]);
+  const T *src = x + (int64_t)(slot / fan_out) * d;
+  T *dst = reinterpret_cast<T *>(peer_rows[q]) + j * d;
+  const float w = weights ? weights[slot] : 1.0f;
+  constexpr int N = 16 / sizeof(T);
+  for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+    uint4 raw = __ldg(reinterpret_cast<const uint4 *>(src + c));
+    if (weights) {
+      T *v = reinterpret_cast<T *>(&raw);
+#pragma unroll
+      for (int u = 0; u < N; ++u) v[u] = Num<T>::from_f(Num<T>::to_f(v[u]) * w);
+    }
+    *reinterpret_cast<uint4 *>(dst + c) = raw;
+  }
+  if (lane == 0 && peer_slot) {
+    reinterpret_cast<int32_t *>(peer_slot[q])[j] = slot;
+    reinterpret_cast<int32_t *>(peer_src[q])[j] = me;
+  }
+}
+
+// local row j -> the source rank's slot-ordered buffer, row recv_slot[j]
+template <typename T>
+__global__ void __launch_bounds__(kThreads) return_kernel(const T *__restrict__ y, int64_t d, int64_t n,
+                                                          const int32_t *__restrict__ recv_slot,
+                                                          const int32_t *__restrict__ recv_src,
+                                                          const uint64_t *__restrict__ peer_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (j >= n) return;
+  const T *src = y + j * d;
+  T *dst = reinterpret_cast<T *>(peer_out[recv_src[j]]) + (int64_t)recv_slot[j] * d;
+  constexpr int N = 16 / sizeof(T);
+  for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N)
+    *reinterpret_cast<uint4 *>(dst + c) = __ldg(reinterpret_cast<const uint4 *>(src + c));
+}
+
+// copy `bytes` (multiple of 4) to every peer at the same byte offset
+__global__ void put_kernel(const uint32_t *__restrict__ src, int64_t words, const uint64_t *__restrict__ peer_dst,
+                           int64_t offset_bytes) {
+  uint32_t *dst = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(peer_dst[blockIdx.x]) + offset_bytes);
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+}
+
+__global__ void signal_kernel(const uint64_t *__restrict__ peer_flags, int world, int me, int slot) {
+  const int q = threadIdx.x;
+  if (q >= world) return;
+  __threadfence_system();
+  unsigned long long *f = reinterpret_cast<unsigned long long *>(peer_flags[q]) + (int64_t)slot * world + me;
+  atomicAdd_system(f, 1ull);
+}
+
+__global__ void wait_kernel(const uint64_t *flags, int world, int slot, uint64_t target, int64_t timeout_ns,
+                            int32_t *err) {
+  const int s = threadIdx.x;
+  if (s >= world) return;
+  const volatile unsigned long long *f =
+      reinterpret_cast<const volatile unsigned long long *>(flags) + (int64_t)slot * world + s;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*f < target) {
+    __nanosleep(256);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if ((int64_t)(t - t0) > timeout_ns) {
+      atomicExch(err, 1);
+      return;
+    }
+  }
+  __threadfence_system();
+}
+
+inline unsigned row_blocks(int64_t rows) { return (unsigned)((rows + kWarps - 1) / kWarps); }
+inline bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace
+}  // namespace smoe
+
+using namespace smoe;
+
+extern "C" {
+
+size_t smoe_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int smoe_ipc_get_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return fail(SMOE_EINVAL, "ipc_get_handle: null pointer");
+  // the handle names the whole allocation (a caching allocator hands out
+  // sub-ranges): report where dev_ptr sits inside it
+  using AddressRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static AddressRangeFn range_fn = nullptr;
+  if (!range_fn) {
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(SMOE_ECUDA, "cuMemGetAddressRange entry point unavailable");
+    range_fn = (AddressRangeFn)fp;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+    return fail(SMOE_ECUDA, "cuMemGetAddressRange failed");
+  *offset_out = (int64_t)((CUdeviceptr)dev_ptr - base);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+  if (e != cudaSuccess) return fail(SMOE_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  memcpy(handle_out, &h, sizeof(h));
+  return SMOE_OK;
+}
+
+int smoe_ipc_open(const void *handle, void **dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(SMOE_EINVAL, "ipc_open: null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(SMOE_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  return SMOE_OK;
+}
+
+int smoe_ipc_close(void *dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return fail(SMOE_ECUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+  return SMOE_OK;
+}
+
+int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_t *order,
+                          const int32_t *sorted_expert, const int32_t *bin_offsets, int32_t fan_out,
+                          const float *weights, int64_t n, const int64_t *dstart, int32_t experts_per_rank,
+                          const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src,
+                          int32_t me, int32_t dtype, void *stream) {
+  if (fan_out < 1 || experts_per_rank < 1) return fail(SMOE_EINVAL, "ep_dispatch: fan_out and experts_per_rank >= 1");
+  if (x_rows * fan_out != n) return fail(SMOE_ESHAPE, "ep_dispatch: x rows * fan_out must equal the slot count");
+  if (n == 0 || d == 0) return SMOE_OK;
+  if (!x || !order || !sorted_expert || !bin_offsets || !dstart || !peer_rows)
+    return fail(SMOE_EINVAL, "ep_dispatch: null pointer");
+  if ((peer_slot == nullptr) != (peer_src == nullptr))
+    return fail(SMOE_EINVAL, "ep_dispatch: peer_slot and peer_src go together");
+  const size_t esz = dtype == SMOE_BF16 ? 2 : 4;
+  if (!al16(x) || (d * (int64_t)esz) % 16) return fail(SMOE_ENOTSUP, "ep_dispatch: rows must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == SMOE_BF16)
+    dispatch_kernel<__nv_bfloat16><<<row_blocks(n), kThreads, 0, st>>>(
+        (const __nv_bfloat16 *)x, d, order, sorted_expert, bin_offsets, fan_out, weights, n, dstart,
+        experts_per_rank, peer_rows, peer_slot, peer_src, me);
+  else if (dtype == SMOE_F32)
+    dispatch_kernel<float><<<row_blocks(n), kThreads, 0, st>>>((const float *)x, d, order, sorted_expert,
+                                                               bin_offsets, fan_out, weights, n, dstart,
+                                                               experts_per_rank, peer_rows, peer_slot, peer_src, me);
+  else
+    return fail(SMOE_EINVAL, "ep_dispatch: unsupported dtype");
+  return check_launch("ep_dispatch_rows");
+}
+
+int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv_slot, const int32_t *recv_src,
+                        const uint64_t *peer_out, int32_t dtype, void *stream) {
+  if (n == 0 || d == 0) return SMOE_OK;
+  if (!y || !recv_slot || !recv_src || !peer_out) return fail(SMOE_EINVAL, "ep_return: null pointer");
+  const size_t esz = dtype == SMOE_BF16 ? 2 : 4;
+  if (!al16(y) || (d * (int64_t)esz) % 16) return fail(SMOE_ENOTSUP, "ep_return: rows must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == SMOE_BF16)
+    return_kernel<__nv_bfloat16><<<row_blocks(n), kThreads, 0, st>>>((const __nv_bfloat16 *)y, d, n, recv_slot,
+                                                                       recv_src, peer_out);
+  else if (dtype == SMOE_F32)
+    return_kernel<float><<<row_blocks(n), kThreads, 0, st>>>((const float *)y, d, n, recv_slot, recv_src, peer_out);
+  else
+    return fail(SMOE_EINVAL, "ep_return: unsupported dtype");
+  return check_launch("ep_return_rows");
+}
+
+int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,
+                void *stream) {
+  if (bytes % 4 || offset_bytes % 4) return fail(SMOE_EINVAL, "ep_put: sizes must be multiples of 4 bytes");
+  if (bytes == 0) return SMOE_OK;
+  put_kernel<<<world, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>((const uint32_t *)src, bytes / 4, peer_dst,
+                                                                         offset_bytes);
+  return check_launch("ep_put");
+}
+
+int smoe_ep_signal(const uint64_t *peer_flags, int32_t world, int32_t me, int32_t slot, void *stream) {
+  if (world < 1 || world > 1024 || me < 0 || me >= world) return fail(SMOE_EINVAL, "ep_signal: bad rank");
+  signal_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(peer_flags, world, me, slot);
+  return check_launch("ep_signal");
+}
+
+int smoe_ep_wait(const uint64_t *flags, int32_t world, int32_t slot, uint64_t target, int64_t timeout_ns,
+                 int32_t *err, void *stream) {
+  if (world < 1 || world > 1024 || !err) return fail(SMOE_EINVAL, "ep_wait: bad arguments");
+  wait_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags, world, slot, target, timeout_ns, err);
+  return check_launch("ep_wait");
+}
+
+}  // extern "C"

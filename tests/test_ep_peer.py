@@ -1,0 +1,135 @@
+"""Expert parallelism over peer memory (paper_2403_08245_b200.ep_peer).
+
+* CPU: the dispatch layout (dstart / local offsets) places every (source,
+  expert, row) at its position in the owner's local grouped order — the order
+  ``ep.local_order_from_counts`` defines for the NCCL path.
+* GPU (one B200, 2 or 4 processes sharing it): ranks map each other's buffers by
+  CUDA IPC and exchange rows with the store kernels — the same kernels and
+  flags protocol as over NVLink — and every output and gradient is
+  bit-identical to one process running the concatenated batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,e", [(2, 4), (4, 8), (3, 6)])
+def test_dispatch_layout_matches_local_grouped_order(world, e):
+    from paper_2403_08245_b200.ep import local_order_from_counts
+    from paper_2403_08245_b200.ep_peer import dispatch_layout
+    rng = np.random.default_rng(world * 10 + e)
+    counts = torch.from_numpy(rng.integers(0, 5, (world, e)))
+    el = e // world
+    for q in range(world):
+        # NCCL path: recv rows source-major (each source's rows for q's experts in expert order)
+        seg = counts[:, q * el:(q + 1) * el]
+        o_loc, off = local_order_from_counts(seg)
+        # position in recv layout of (s, local expert, u)
+        recv_pos = {}
+        base = 0
+        for s in range(world):
+            for le in range(el):
+                for u in range(int(seg[s, le])):
+                    recv_pos[(s, le, u)] = base
+                    base += 1
+        want = {recv_pos[key]: None for key in recv_pos}
+        inv = {int(r): i for i, r in enumerate(o_loc.tolist())}   # recv position -> local grouped position
+        for s in range(world):
+            dstart, off_q = dispatch_layout(counts, s)
+            for le in range(el):
+                eg = q * el + le
+                for u in range(int(counts[s, eg])):
+                    want[recv_pos[(s, le, u)]] = int(dstart[eg]) + u
+        assert all(inv[r] == pos for r, pos in want.items())
+        _, off_me = dispatch_layout(counts, q)
+        assert off_me.tolist() == off.tolist()
+
+
+T_LOCAL, D, DE, E, K = 512, 256, 512, 8, 2
+
+
+def _problem(world):
+    g = torch.Generator().manual_seed(11)
+    x = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
+    dy = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
+    w1 = ((torch.rand(E, D, DE, generator=g) * 2 - 1) / D ** 0.5).bfloat16()
+    w2 = ((torch.rand(E, DE, D, generator=g) * 2 - 1) / DE ** 0.5).bfloat16()
+    logits = torch.randn(world * T_LOCAL, E, generator=g)
+    logits[:40, 0] += 8.0        # skew: many rows to expert 0 (owned by rank 0)
+    return x, dy, w1, w2, logits
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2403_08245_b200 as sm
+        from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
+        torch.cuda.set_device(0)
+        x, dy, w1, w2, logits = (a.cuda() for a in _problem(world))
+        routing = sm.topk_select(torch.softmax(logits, 1), K)
+        # single-process reference on the concatenated batch
+        order = sm.compute_grouped_order(routing)
+        y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+        g_ref = sm.smoe_mlp_backward(c, dy)
+        sl = slice(rank * T_LOCAL, (rank + 1) * T_LOCAL)
+        el = E // world
+        es = slice(rank * el, (rank + 1) * el)
+        ep = PeerExpertParallelSmoeMlp(w1[es].contiguous(), w2[es].contiguous(), E, K, max_tokens=T_LOCAL,
+                                       timeout_s=120.0)
+        rt = sm.RoutingResult(routing.expert_idx[sl].contiguous(), routing.p[sl].contiguous(),
+                              routing.gate_full[sl].contiguous(), renormalized=True, validate=False)
+        ok = []
+        for it in range(2):      # twice: the second step reuses every buffer
+            y, ctx = ep.forward(x[sl].contiguous(), rt)
+            gr = ep.backward(ctx, dy[sl].contiguous())
+            torch.cuda.synchronize()
+            ep._check_err()
+            ok.append({"y": torch.equal(y, y_ref[sl]), "dx": torch.equal(gr.dx, g_ref.dx[sl]),
+                       "dp": torch.equal(gr.dp, g_ref.dp[sl]), "dw1": torch.equal(gr.dw1, g_ref.dw1[es]),
+                       "dw2": torch.equal(gr.dw2, g_ref.dw2[es])})
+        ep.close()
+        q.put((rank, ok, None))
+    except Exception as exc:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_ep_processes_sharing_one_gpu_bit_identical(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = {}
+    try:
+        for _ in range(world):
+            r = q.get(timeout=300)
+            results[r[0]] = r
+    finally:
+        for pr in procs:
+            pr.join(timeout=60)
+            if pr.is_alive():
+                pr.kill()
+    for rank in range(world):
+        _, ok, err = results[rank]
+        assert err is None, err
+        for step in ok:
+            assert all(step.values()), (rank, step)
