@@ -210,6 +210,13 @@ int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_
 /* Return: local row j goes to row recv_slot[j] of peer_out[recv_src[j]]. */
 int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv_slot, const int32_t *recv_src,
                         const uint64_t *peer_out, int32_t dtype, void *stream);
+/* The return fused into the expert GEMM: out_j = x_j @ W[e] (or W[e]^T) for the
+ * grouped rows x [n, d_in] (bins = expert_offsets), each output row stored by
+ * the GEMM epilogue straight into row recv_slot[j] of peer_out[recv_src[j]]
+ * (bf16, tcgen05 CTA-pair engine). */
+int smoe_ep_gemm_return(const void *x, int64_t n, const void *w, int32_t num_experts, int64_t w_rows, int64_t w_cols,
+                        const int32_t *expert_offsets, int32_t transpose_w, const int32_t *recv_slot,
+                        const int32_t *recv_src, const uint64_t *peer_out, void *stream);
 /* Copy `bytes` from src to every peer_dst[q] + offset_bytes. */
 int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,
                 void *stream);

@@ -51,6 +51,7 @@ SIGNATURES = {
     "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp,
                                          _i32, _i32, _vp]),
     "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_ep_gemm_return": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "smoe_ep_put": (_c.c_int, [_vp, _i64, _vp, _i64, _i32, _vp]),
     "smoe_ep_signal": (_c.c_int, [_vp, _i32, _i32, _i32, _vp]),
     "smoe_ep_wait": (_c.c_int, [_vp, _i32, _i32, _c.c_uint64, _i64, _vp, _vp]),

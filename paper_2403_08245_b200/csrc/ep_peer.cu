@@ -120,6 +120,11 @@ inline unsigned row_blocks(int64_t rows) { return (unsigned)((rows + kWarps - 1)
 inline bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 }  // namespace
+
+bool tc_available();
+int tc_scatter2scatter_peer(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                            const int32_t *, int64_t, int, const uint64_t *, const int32_t *, const int32_t *,
+                            cudaStream_t);
 }  // namespace smoe
 
 using namespace smoe;
@@ -212,6 +217,19 @@ int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv
   else
     return fail(SMOE_EINVAL, "ep_return: unsupported dtype");
   return check_launch("ep_return_rows");
+}
+
+int smoe_ep_gemm_return(const void *x, int64_t n, const void *w, int32_t num_experts, int64_t w_rows, int64_t w_cols,
+                        const int32_t *expert_offsets, int32_t transpose_w, const int32_t *recv_slot,
+                        const int32_t *recv_src, const uint64_t *peer_out, void *stream) {
+  if (n == 0) return SMOE_OK;
+  if (!x || !w || !expert_offsets || !recv_slot || !recv_src || !peer_out)
+    return fail(SMOE_EINVAL, "ep_gemm_return: null pointer");
+  if (!tc_available()) return fail(SMOE_ENOTSUP, "ep_gemm_return: needs the tcgen05 engine");
+  // grouped input: the order array is only read for scattered layouts; the
+  // bin offsets drive the tile schedule
+  return tc_scatter2scatter_peer(x, n, w, num_experts, w_rows, w_cols, recv_slot, expert_offsets, n, transpose_w,
+                                 peer_out, recv_src, recv_slot, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,

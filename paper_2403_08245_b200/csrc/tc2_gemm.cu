@@ -437,7 +437,12 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         const bool slab_tma = tma_out && slab0 + 32 <= tl.m_end;
         const int slab_row = (int)(GK ? (int64_t)tl.e * p.M + slab0 : slab0);
         long long dst = -1;
-        if (row < tl.m_end) dst = GK ? (int64_t)tl.e * p.M + row : (p.grouped_out ? row : (int64_t)p.order[row]);
+        if (row < tl.m_end) {
+          if (!GK && p.peer_out)  // absolute address of the row in its owner's buffer
+            dst = (long long)(p.peer_out[p.row_src[row]] + (uint64_t)p.row_slot[row] * (uint64_t)p.N * 2u);
+          else
+            dst = GK ? (int64_t)tl.e * p.M + row : (p.grouped_out ? row : (int64_t)p.order[row]);
+        }
         long long cdst[8];
   #pragma unroll
         for (int i = 0; i < 8; ++i) cdst[i] = __shfl_sync(0xffffffffu, dst, cr + 4 * i);
@@ -546,7 +551,8 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
               __syncwarp();
             } else {
               __syncwarp();
-              store_staged_rows(stg, pass == 0 ? p.out : p.out2, cdst, col0, col_ok, p.N, cr, cc);
+              store_staged_rows(stg, (!GK && p.peer_out) ? nullptr : (pass == 0 ? p.out : p.out2), cdst, col0, col_ok,
+                                p.N, cr, cc);
             }
           }
         }
@@ -881,7 +887,8 @@ static bool encode_out_map(CUtensorMap *m, const void *ptr, int64_t rows, int64_
 static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
                     const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout, int trans,
                     int epi, int act, void *out, void *out2, const void *aux, const float *pw, float *yacc,
-                    int combine_cols, cudaStream_t st) {
+                    int combine_cols, cudaStream_t st, const uint64_t *peer_out = nullptr,
+                    const int32_t *row_src = nullptr, const int32_t *row_slot = nullptr) {
   const int64_t d_in = trans ? w_cols : w_rows;
   const int64_t d_out = trans ? w_rows : w_cols;
   CUtensorMap ta, tb;
@@ -914,6 +921,9 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.x = (const __nv_bfloat16 *)x;
   p.pw = pw;
   p.yacc = yacc;
+  p.peer_out = peer_out;
+  p.row_src = row_src;
+  p.row_slot = row_slot;
   p.combine_cols = combine_cols;
   p.group_m = band_rows(d_in);
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
@@ -924,7 +934,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
-    if (epi == EPI_COMBINE || staged_for(false, gout, d_in)) {
+    if (epi == EPI_COMBINE || peer_out || staged_for(false, gout, d_in)) {
       if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
       return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
     }
@@ -940,6 +950,16 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
                     int epi, int act, void *out, void *out2, const void *aux, cudaStream_t st) {
   return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi, act, out, out2,
                   aux, nullptr, nullptr, 1, st);
+}
+
+// Grouped-input GEMM whose epilogue stores output row i straight into row
+// row_slot[i] of rank row_src[i]'s buffer (peer memory): the expert-parallel
+// return fused into the expert GEMM (ep_peer.py).
+int scatter2scatter_peer(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                         const int32_t *order, const int32_t *offsets, int64_t n, int trans, const uint64_t *peer_out,
+                         const int32_t *row_src, const int32_t *row_slot, cudaStream_t st) {
+  return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, 1, 1, 0, trans, SMOE_EPI_NONE, 0, nullptr,
+                  nullptr, nullptr, nullptr, nullptr, 1, st, peer_out, row_src, row_slot);
 }
 
 // scatter_combine (kernels.py:242-286): scattered-output GEMM whose epilogue

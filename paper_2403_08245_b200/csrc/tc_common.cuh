@@ -41,6 +41,11 @@ struct Params {
   int combine_cols;        // EPI_COMBINE: slots per output row
   const __nv_bfloat16 *y;  // B_ROWS_MN_G: the scattered B rows [y_rows, N]
   int fan_out_b;           // B_ROWS_MN_G: slots per B row
+  // Peer-store epilogue (expert-parallel return): output row i goes to row
+  // row_slot[i] of the buffer at peer_out[row_src[i]] (another rank's memory).
+  const uint64_t *peer_out;
+  const int32_t *row_src;
+  const int32_t *row_slot;
 };
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -475,13 +480,17 @@ __device__ __forceinline__ void epilogue_pack32(const Params &p, const uint32_t 
 // XOR-swizzled by row) to global: lane (cr, cc) writes chunk cc of rows
 // cr + 4 i to row cdst[i] (< 0: masked) of `base` — 4 full 128-byte row
 // segments per store instruction instead of 32 scattered 16-byte pieces.
+// With base == nullptr, cdst[i] is the row's absolute byte address (peer rows).
 __device__ __forceinline__ void store_staged_rows(uint32_t stg, __nv_bfloat16 *base, const long long (&cdst)[8],
                                                   int64_t col0, bool col_ok, int64_t ld, int cr, int cc) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int rl = cr + 4 * i;
     const uint4 val = lds128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4));
-    if (cdst[i] >= 0 && col_ok) *reinterpret_cast<uint4 *>(base + cdst[i] * ld + col0 + cc * 8) = val;
+    if (cdst[i] >= 0 && col_ok) {
+      __nv_bfloat16 *rowp = base ? base + cdst[i] * ld : reinterpret_cast<__nv_bfloat16 *>(cdst[i]);
+      *reinterpret_cast<uint4 *>(rowp + col0 + cc * 8) = val;
+    }
   }
   __syncwarp();
 }

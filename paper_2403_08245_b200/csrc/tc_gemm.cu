@@ -406,6 +406,9 @@ int scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, 
                     int64_t, int, int, const float *, int, float *, cudaStream_t);
 int group_xty_scattered(const void *, int64_t, int, int, const void *, int64_t, int, int, const int32_t *,
                         const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+int scatter2scatter_peer(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                         const int32_t *, int64_t, int, const uint64_t *, const int32_t *, const int32_t *,
+                         cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -495,6 +498,17 @@ int tc_scatter_combine(const void *x, int64_t x_rows, const void *w, int E, int6
 
 // gathered rows are addressed by 31-bit offsets in 16-byte chunks
 static bool xty_offsets_fit(int64_t rows, int64_t cols) { return rows * (cols / 8) < (1ll << 31); }
+
+int tc_scatter2scatter_peer(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                            const int32_t *order, const int32_t *offsets, int64_t n, int trans,
+                            const uint64_t *peer_out, const int32_t *row_src, const int32_t *row_slot,
+                            cudaStream_t st) {
+  const int64_t d_in = trans ? w_cols : w_rows, d_out = trans ? w_rows : w_cols;
+  if (!(tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && tc_supports_s2s(d_in, d_out, x, w, x)))
+    return fail(SMOE_ENOTSUP, "peer-store GEMM needs the CTA-pair engine, d_in, d_out multiples of 8");
+  return tc2::scatter2scatter_peer(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, trans, peer_out, row_src,
+                                   row_slot, st);
+}
 
 // group_xty with scattered (gathered) operands: CTA-pair kernels only.
 bool tc_supports_xty_scattered(int E, int64_t x_rows, int64_t d_in, int64_t y_rows, int64_t d_out, const void *x,

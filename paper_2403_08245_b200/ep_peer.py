@@ -15,14 +15,17 @@ all-to-all and no pack / unpack copies:
                dstart[e] + (i - off[e]) of the owner's receive buffer — its
                final position in the owner's local grouped order — together
                with its slot id and the source rank;
-            4. the owner runs layer 1 and layer 2 on the received rows as they
-               landed (grouped in, grouped out: TMA-fed, no group() copy);
-            5. return kernel: output row j goes straight to row slot[j] of its
-               source's slot-ordered buffer; the source combines with p.
+            4. the owner runs layer 1 on the received rows as they landed
+               (grouped in, grouped out: TMA-fed, no group() copy);
+            5. layer 2's GEMM epilogue stores output row j straight into row
+               slot[j] of its source's slot-ordered buffer (the combine-side
+               all-to-all fused into the expert GEMM); the source combines
+               with p.
   backward  p-weighted dY rows are dispatched to the same positions; the
             owner's dW2, dH, dW1 and slot input-gradients run on grouped rows
-            only (dW stays local: no all-reduce); the slot gradients return to
-            the source, which reduces over the k slots.
+            only (dW stays local: no all-reduce); the input-gradient GEMM's
+            epilogue stores the slot gradients into the source's buffer, which
+            reduces over the k slots.
 
 Peer buffers are CUDA IPC mappings of each rank's buffers (``SymmetricBuffer``);
 the store kernels write through NVLink P2P on a multi-GPU box and into the
@@ -33,6 +36,7 @@ that exceeds ``timeout_s`` raises instead of hanging the device.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -46,6 +50,10 @@ from .router import GroupedOrder, RoutingResult, compute_grouped_order
 # flag slots: one counter per (slot, source rank) on every rank
 _READY, _COUNTS, _FWD_DISPATCH, _FWD_RETURN, _BWD_DISPATCH, _BWD_RETURN = range(6)
 _NUM_SLOTS = 6
+
+# The return is fused into the expert GEMM (its epilogue stores each output row
+# into the source's buffer); SMOE_EP_FUSED_RETURN=0 runs GEMM + return kernel.
+_FUSED_RETURN = os.environ.get("SMOE_EP_FUSED_RETURN", "1") != "0"
 
 
 def _stream() -> int:
@@ -233,11 +241,9 @@ class PeerExpertParallelSmoeMlp:
         h = torch.empty_like(h_pre)
         K.scatter2scatter(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, out=h_pre, activation=self.activation,
                           act_out=h)
-        y_loc = K.scatter2scatter(h, self.w2, order_loc, 1, GROUPED_TO_GROUPED)
-        # 5. outputs back to their source slots, then the routing-weighted combine
-        _lib.check(lib.smoe_ep_return_rows(
-            y_loc.data_ptr(), n_recv, self.d, self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr(),
-            self.y_ret.peers.data_ptr(), _lib.SMOE_BF16, _stream()), "ep_return_rows")
+        # 5. layer 2, its outputs stored back into their source slots; then the
+        #    routing-weighted combine at the source
+        self._gemm_return(h, self.w2, order_loc, False, self.y_ret)
         self._exchange_done(_FWD_RETURN)
         y_slot = self.y_ret.view(torch.bfloat16, (self.max_tokens * k, self.d))[:n]
         y = K.combine(routing.p, y_slot)
@@ -266,14 +272,27 @@ class PeerExpertParallelSmoeMlp:
         dh = K.scatter2scatter(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=ctx.h,
                                activation=ctx.activation, act_grad_of=ctx.h_pre)
         dw1 = K.group_xty(r, dh, ol)
-        dr = K.scatter2scatter(dh, self.w1, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=dyl)
-        _lib.check(lib.smoe_ep_return_rows(
-            dr.data_ptr(), nr, self.d, self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr(),
-            self.dx_ret.peers.data_ptr(), _lib.SMOE_BF16, _stream()), "ep_return_rows")
+        self._gemm_return(dh, self.w1, ol, True, self.dx_ret, scratch=dyl)
         self._exchange_done(_BWD_RETURN)
         dx_slot = self.dx_ret.view(torch.bfloat16, (self.max_tokens * k, self.d))[:n]
         dx = K.fanout_reduce(dx_slot, k)
         return PeerEpGradients(dx=dx, dw1=dw1, dw2=dw2, dp=dp)
+
+    def _gemm_return(self, a: torch.Tensor, w: torch.Tensor, order_loc: GroupedOrder, transpose: bool,
+                     dest: SymmetricBuffer, scratch: torch.Tensor | None = None) -> None:
+        """rows a @ W[e] (W[e]^T) of the local grouped order, each stored into its
+        source's slot row of `dest` — in the GEMM epilogue when fused."""
+        lib = _lib.load()
+        n = a.shape[0]
+        slot, src = self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr()
+        if _FUSED_RETURN:
+            _lib.check(lib.smoe_ep_gemm_return(a.data_ptr(), n, w.data_ptr(), w.shape[0], w.shape[1], w.shape[2],
+                                               order_loc.bin_offsets.data_ptr(), int(transpose), slot, src,
+                                               dest.peers.data_ptr(), _stream()), "ep_gemm_return")
+            return
+        out = K.scatter2scatter(a, w, order_loc, 1, GROUPED_TO_GROUPED, transpose_w=transpose, out=scratch)
+        _lib.check(lib.smoe_ep_return_rows(out.data_ptr(), n, self.d, slot, src, dest.peers.data_ptr(),
+                                           _lib.SMOE_BF16, _stream()), "ep_return_rows")
 
     def close(self) -> None:
         torch.cuda.synchronize()

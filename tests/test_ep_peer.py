@@ -70,7 +70,8 @@ def _problem(world):
     return x, dy, w1, w2, logits
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, fused="1"):
+    os.environ["SMOE_EP_FUSED_RETURN"] = fused
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -110,12 +111,13 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 4])
-def test_peer_ep_processes_sharing_one_gpu_bit_identical(world):
+@pytest.mark.parametrize("world,fused", [(2, "1"), (4, "1"), (2, "0")])
+def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused):
+    """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused)) for r in range(world)]
     for pr in procs:
         pr.start()
     results = {}
