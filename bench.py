@@ -200,11 +200,17 @@ def run_ours(args, rank, world, local_rank):
     ep_mode = args.ep if args.ep != "auto" else ("peer" if world > 1 else "none")
     if ep_mode != "none":
         # expert parallelism: this rank owns experts [rank*E/G, (rank+1)*E/G)
+        ep = None
         if ep_mode == "peer":
             # rows stored straight into the owner's buffers over peer memory (ep_peer.py)
             from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
-            ep = PeerExpertParallelSmoeMlp(w1, w2, E, k, max_tokens=T)
-        else:
+            try:
+                ep = PeerExpertParallelSmoeMlp(w1, w2, E, k, max_tokens=T)
+            except RuntimeError as exc:   # raised on every rank together
+                if rank == 0:
+                    print(f"bench: {exc}; falling back to the NCCL exchange", file=sys.stderr)
+                ep_mode = "nccl"
+        if ep is None:
             from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
             ep = ExpertParallelSmoeMlp(w1, w2, E)
 

@@ -79,13 +79,17 @@ class SymmetricBuffer:
         gathered = [None] * self.world
         dist.all_gather_object(gathered, (handle.raw, offset.value), group=group)
         self._opened: list[int] = []
+        self.error: str | None = None     # a failed mapping is reported collectively by the owner
         ptrs = []
         for q, (raw, off) in enumerate(gathered):
             if q == self.rank:
                 ptrs.append(self.local.data_ptr())
                 continue
             base = ctypes.c_void_p()
-            _lib.check(lib.smoe_ipc_open(raw, ctypes.byref(base)), "ipc_open")
+            if lib.smoe_ipc_open(raw, ctypes.byref(base)) != 0:
+                self.error = f"rank {self.rank}: cannot map rank {q}'s buffer: {_lib.last_error()}"
+                ptrs.append(0)
+                continue
             self._opened.append(base.value)
             ptrs.append(base.value + off)
         self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
@@ -187,6 +191,17 @@ class PeerExpertParallelSmoeMlp:
         self.dx_ret = SymmetricBuffer(esz * slots * d, dev, group)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = [0] * _NUM_SLOTS
+        # every rank must have mapped every peer buffer; decide collectively so
+        # all ranks raise together (a caller can then fall back to ep.py)
+        bufs = (self.flags, self.counts, self.recv_x, self.recv_dy, self.recv_slot, self.recv_src, self.y_ret,
+                self.dx_ret)
+        errors = [b.error for b in bufs if b.error]
+        gathered = [None] * g
+        dist.all_gather_object(gathered, errors[0] if errors else None, group=group)
+        bad = [e for e in gathered if e]
+        if bad:
+            self.close()
+            raise RuntimeError("peer-memory EP unavailable: " + "; ".join(bad))
 
     # ---- completion ------------------------------------------------------------
     def _exchange_done(self, slot: int) -> None:
