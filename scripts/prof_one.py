@@ -33,6 +33,10 @@ for _ in range(3):
                            activation="gelu", act_grad_of=h)
     elif which == "gather":
         sm.scatter2scatter(x, w, order, k, sm.SCATTERED_TO_GROUPED, out=h)
+    elif which == "gathers":  # gather, scattered output (S->S)
+        sm.scatter2scatter(x, w, order, k, sm.SCATTERED_TO_SCATTERED, out=h)
+    elif which == "rowss":  # TMA rows, scattered output (G->S)
+        sm.scatter2scatter(xg, w, order, 1, sm.GROUPED_TO_SCATTERED, out=h)
     elif which == "dhnone":
         sm.scatter2scatter(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, out=h2)
     elif which == "dx":

@@ -56,10 +56,11 @@ def test_dispatch_layout_matches_local_grouped_order(world, e):
         assert off_me.tolist() == off.tolist()
 
 
-T_LOCAL, D, DE, E, K = 512, 256, 512, 8, 2
+T_LOCAL, D, DE = 512, 256, 512
+SHAPES = {"c1": (8, 2), "c4": (64, 8)}     # (E, k): Mixtral-like and the fine-grained EP config
 
 
-def _problem(world):
+def _problem(world, E):
     g = torch.Generator().manual_seed(11)
     x = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
     dy = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
@@ -70,15 +71,16 @@ def _problem(world):
     return x, dy, w1, w2, logits
 
 
-def _worker(rank, world, port, q, fused="1"):
+def _worker(rank, world, port, q, fused="1", shape="c1"):
     os.environ["SMOE_EP_FUSED_RETURN"] = fused
+    E, K = SHAPES[shape]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2403_08245_b200 as sm
         from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
         torch.cuda.set_device(0)
-        x, dy, w1, w2, logits = (a.cuda() for a in _problem(world))
+        x, dy, w1, w2, logits = (a.cuda() for a in _problem(world, E))
         routing = sm.topk_select(torch.softmax(logits, 1), K)
         # single-process reference on the concatenated batch
         order = sm.compute_grouped_order(routing)
@@ -111,13 +113,13 @@ def _worker(rank, world, port, q, fused="1"):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,fused", [(2, "1"), (4, "1"), (2, "0")])
-def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused):
+@pytest.mark.parametrize("world,fused,shape", [(2, "1", "c1"), (4, "1", "c1"), (2, "0", "c1"), (4, "1", "c4")])
+def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shape)) for r in range(world)]
     for pr in procs:
         pr.start()
     results = {}
