@@ -53,7 +53,11 @@ typedef enum {
   SMOE_EPI_NONE = 0,     /* out[dst] = acc                                          */
   SMOE_EPI_ACT = 1,      /* out[dst] = pre = acc;  out2[dst] = act(pre)             */
   SMOE_EPI_ACT_GRAD = 2, /* out[dst] = acc * act'(aux[dst])   (aux = h_pre)         */
-  SMOE_EPI_ACT_ONLY = 3  /* out[dst] = act(acc)  (inference: no pre-activation kept)  */
+  SMOE_EPI_ACT_ONLY = 3, /* out[dst] = act(acc)  (inference: no pre-activation kept)  */
+  /* smoe_scatter2scatter_scaled only (row i's scale s = row_scale[order[i]]): */
+  SMOE_EPI_ACT_SCALED = 4,     /* out = pre = acc;  out2 = s * act(pre)                      */
+  SMOE_EPI_ACT_GRAD_SCALED = 5 /* out = s * acc * act'(aux);  dp_part[i, part] =
+                                  sum over the part's columns of acc * act(aux)                */
 } smoe_epilogue;
 
 /* GEMM engine selection: AUTO picks tcgen05 for bf16 and the SIMT fp32 kernel
@@ -150,6 +154,28 @@ int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, 
  *   apply: out = act(x);  grad: out = act'(x)                            */
 int smoe_apply_activation(const void *x, int64_t numel, int32_t activation, int32_t derivative,
                     int32_t dtype, void *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Routing-weight-scaled epilogues of the SMoE MLP (moe_layers.py:140-211 with
+ * the combine weight moved through the second GEMM, bf16, tcgen05 CTA-pair
+ * engine): SMOE_EPI_ACT_SCALED writes the hidden state already multiplied by
+ * its slot's routing weight, so layer 2 + an unweighted k-sum is the combine
+ * (parallel_linear.py:69-73); SMOE_EPI_ACT_GRAD_SCALED produces the hidden
+ * gradient and, from the same accumulators, the combine-weight gradient's
+ * partial dot products (dp[s] = <dY W2^T, act(h_pre)>, parallel_linear.py:198-206)
+ * without the retained layer-2 output.  dp_part is [n, dp_parts] fp32,
+ * dp_parts = 2 * ceil(d_out / 256); smoe_dp_from_partials reduces it.
+ */
+int smoe_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                                int64_t w_rows, int64_t w_cols, const int32_t *order,
+                                const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                                int32_t grouped_in, int32_t grouped_out, int32_t transpose_w,
+                                int32_t epilogue, int32_t activation, const float *row_scale, void *out,
+                                void *out2, const void *aux, float *dp_part, int32_t dp_parts, void *stream);
+int32_t smoe_dp_parts(int64_t d_out);
+/* dp[order[i]] = sum_j dp_part[i * parts + j]  (dp: n floats in slot order) */
+int smoe_dp_from_partials(const float *dp_part, int64_t n, int32_t parts, const int32_t *order, float *dp,
+                          void *stream);
 
 /* ---------------------------------------------------------------------------
  * group_xty over scattered operands: the reference's group() + group_xty()

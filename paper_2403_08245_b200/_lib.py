@@ -21,7 +21,7 @@ LIB_PATH = Path(os.environ["SMOE_LIB"]) if os.environ.get("SMOE_LIB") else _PKG 
 SMOE_OK, SMOE_EINVAL, SMOE_ESHAPE, SMOE_ECUDA, SMOE_ENOTSUP = range(5)
 SMOE_F32, SMOE_BF16 = 0, 1
 ACTIVATION_IDS = {"gelu": 0, "relu": 1, "silu": 2}
-EPI_NONE, EPI_ACT, EPI_ACT_GRAD, EPI_ACT_ONLY = 0, 1, 2, 3
+EPI_NONE, EPI_ACT, EPI_ACT_GRAD, EPI_ACT_ONLY, EPI_ACT_SCALED, EPI_ACT_GRAD_SCALED = 0, 1, 2, 3, 4, 5
 ENGINE_IDS = {"auto": 0, "simt": 1, "tcgen05": 2}
 
 _c = ctypes
@@ -51,6 +51,10 @@ SIGNATURES = {
     "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp,
                                          _i32, _i32, _vp]),
     "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_scatter2scatter_scaled": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
+                                               _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_dp_parts": (_i32, [_i64]),
+    "smoe_dp_from_partials": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "smoe_ep_gemm_return": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "smoe_ep_put": (_c.c_int, [_vp, _i64, _vp, _i64, _i32, _vp]),
     "smoe_ep_signal": (_c.c_int, [_vp, _i32, _i32, _i32, _vp]),

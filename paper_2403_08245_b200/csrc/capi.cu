@@ -31,6 +31,10 @@ int group(const void *, int64_t, const int32_t *, int64_t, int, const float *, i
 int combine(const void *, const float *, int64_t, int, int64_t, int, void *, cudaStream_t);
 int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, float *, cudaStream_t);
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
+int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                              const int32_t *, int64_t, int, int, int, int, int, int, const float *, void *, void *,
+                              const void *, float *, int, cudaStream_t);
 int activation(const void *, int64_t, int, int, int, void *, cudaStream_t);
 int simt_scatter2scatter(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int simt_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int, void *, cudaStream_t);
@@ -203,6 +207,42 @@ int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32
   if (s_rows == 0) return SMOE_OK;
   REQUIRE(dy && y_hat && dp, SMOE_EINVAL, "combine_grad_p: null pointer");
   return combine_grad_p(dy, y_hat, s_rows, j_cols, d, dtype, dp, S(stream));
+}
+
+int32_t smoe_dp_parts(int64_t d_out) { return (int32_t)(2 * ((d_out + 255) / 256)); }
+
+int smoe_dp_from_partials(const float *dp_part, int64_t n, int32_t parts, const int32_t *order, float *dp,
+                          void *stream) {
+  REQUIRE(parts >= 1, SMOE_EINVAL, "dp_from_partials: parts must be >= 1");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(dp_part && order && dp, SMOE_EINVAL, "dp_from_partials: null pointer");
+  return dp_from_partials(dp_part, n, parts, order, dp, S(stream));
+}
+
+int smoe_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
+                                int64_t w_rows, int64_t w_cols, const int32_t *order,
+                                const int32_t *expert_offsets, int64_t n, int32_t fan_out,
+                                int32_t grouped_in, int32_t grouped_out, int32_t transpose_w,
+                                int32_t epilogue, int32_t activation, const float *row_scale, void *out,
+                                void *out2, const void *aux, float *dp_part, int32_t dp_parts, void *stream) {
+  REQUIRE(epilogue == SMOE_EPI_ACT_SCALED || epilogue == SMOE_EPI_ACT_GRAD_SCALED, SMOE_EINVAL,
+          "scatter2scatter_scaled takes SMOE_EPI_ACT_SCALED or SMOE_EPI_ACT_GRAD_SCALED");
+  REQUIRE(activation >= SMOE_ACT_GELU && activation <= SMOE_ACT_SILU, SMOE_EINVAL, "bad activation");
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
+  if (grouped_in)
+    REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");
+  else
+    REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
+  REQUIRE(epilogue != SMOE_EPI_ACT_SCALED || out2, SMOE_EINVAL, "EPI_ACT_SCALED needs out2");
+  REQUIRE(epilogue != SMOE_EPI_ACT_GRAD_SCALED || aux, SMOE_EINVAL, "EPI_ACT_GRAD_SCALED needs aux");
+  const int64_t d_out = transpose_w ? w_rows : w_cols;
+  REQUIRE(!dp_part || dp_parts == smoe_dp_parts(d_out), SMOE_EINVAL, "dp_parts must be smoe_dp_parts(d_out)");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(x && w && order && expert_offsets && out && row_scale, SMOE_EINVAL, "scatter2scatter_scaled: null pointer");
+  REQUIRE(tc_available(), SMOE_ENOTSUP, "scaled epilogues run on the tcgen05 engine");
+  return tc_scatter2scatter_scaled(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
+                                   grouped_in, grouped_out, transpose_w, epilogue, activation, row_scale, out, out2,
+                                   aux, dp_part, dp_parts, S(stream));
 }
 
 int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, int64_t d,

@@ -86,6 +86,18 @@ __device__ __forceinline__ float act_grad_fast(int act, float z) {
   return s * (1.0f + z * (1.0f - s));
 }
 
+// act(z) and act'(z) together (GELU shares one erf / exp evaluation).
+__device__ __forceinline__ void act_both_fast(int act, float z, float &f, float &g) {
+  if (act == SMOE_ACT_GELU) {
+    const ErfExp r = erf_scaled(z);
+    f = 0.5f * z * (1.0f + r.erf);
+    g = fmaf(z * 0.39894228040143268f, r.gexp, 0.5f * (1.0f + r.erf));
+    return;
+  }
+  f = act_fwd_fast(act, z);
+  g = act_grad_fast(act, z);
+}
+
 inline int num_sms() {
   static int sms = -1;
   if (sms < 0) {

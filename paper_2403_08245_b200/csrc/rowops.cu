@@ -239,6 +239,24 @@ int combine_grad_p(const void *dy, const void *y_hat, int64_t S, int J, int64_t 
   return check_launch("combine_grad_p");
 }
 
+// dp[order[i]] = sum_j part[i * parts + j]: one thread per grouped row, the
+// partials summed in a fixed order (deterministic).
+__global__ void dp_from_partials_kernel(const float *__restrict__ part, int64_t n, int parts,
+                                        const int32_t *__restrict__ order, float *__restrict__ dp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float *r = part + i * parts;
+  float s = 0.0f;
+  for (int j = 0; j < parts; ++j) s += r[j];
+  dp[order[i]] = s;
+}
+
+int dp_from_partials(const float *part, int64_t n, int parts, const int32_t *order, float *dp, cudaStream_t st) {
+  if (n == 0) return SMOE_OK;
+  dp_from_partials_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, parts, order, dp);
+  return check_launch("dp_from_partials");
+}
+
 int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx,
                   cudaStream_t st) {
   if (Trows == 0 || d == 0) return SMOE_OK;

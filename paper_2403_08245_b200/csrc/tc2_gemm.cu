@@ -447,6 +447,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   #pragma unroll
         for (int i = 0; i < 8; ++i) cdst[i] = __shfl_sync(0xffffffffu, dst, cr + 4 * i);
         const bool combine = p.epi == EPI_COMBINE;
+        // *_SCALED epilogues: this thread's row scale and combine-weight-gradient partial
+        float rscale = 1.0f, dpacc = 0.0f;
+        if (epi_scaled(p.epi) && dst >= 0) rscale = __ldg(p.pw + p.order[row]);
         float cscale = 0.f;  // combine: this thread's row weight; cdst becomes the token row
         if (combine) {
           if (dst >= 0) cscale = __ldg(p.pw + dst);
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             }
             continue;
           }
-          if (p.epi == SMOE_EPI_ACT_GRAD) {
+          if (epi_act_grad(p.epi)) {
             // coalesced read of the 32 rows' h_pre segments into the staging tile
   #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           }
           // one pass per output (EPI_ACT writes h_pre, then act(h_pre) from a TMEM re-read);
           // each pass builds this lane's 128-byte row segment in two 32-column halves
-          const int passes = (p.epi == SMOE_EPI_ACT) ? 2 : 1;
+          const int passes = (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_SCALED) ? 2 : 1;
           for (int pass = 0; pass < passes; ++pass) {
   #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
                 for (int i = 0; i < 32; ++i) v[i] = 0u;
               }
               uint32_t io[16];
-              if (p.epi == SMOE_EPI_ACT_GRAD) {
+              if (epi_act_grad(p.epi)) {
   #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                   const uint4 val = lds128(stg + lane * 128 + (((4 * hf + c) ^ (lane & 7)) << 4));
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
                 }
               }
               if (has_acc) tmem_ld_wait();
-              epilogue_pack32(p, v, io, pass == 1);
+              epilogue_pack32(p, v, io, pass == 1, rscale, &dpacc);
   #pragma unroll
               for (int c = 0; c < 4; ++c)
                 sts128(stg + lane * 128 + (((4 * hf + c) ^ (lane & 7)) << 4),
@@ -556,6 +559,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             }
           }
         }
+        if (p.dp_part && dst >= 0) p.dp_part[row * p.dp_parts + (tl.n0 / TN) * 2 + warp / 4] = dpacc;
         if (has_acc) {
           tc_fence_before();
           __syncwarp();
@@ -593,7 +597,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         }
         const bool has_acc = tl.nkb > 0;
         uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-        const bool use_aux = (p.epi == SMOE_EPI_ACT_GRAD) && valid;
+        const bool use_aux = epi_act_grad(p.epi) && valid;
+        float rscale = 1.0f, dpacc = 0.0f;
+        if (epi_scaled(p.epi) && valid) rscale = __ldg(p.pw + p.order[row]);
         if (use_aux) {
           const int64_t c0 = tl.n0 + c_begin;
   #pragma unroll
@@ -622,10 +628,11 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
               if (col0 + 16 + 8 * j < p.N) avn[j] = __ldg(reinterpret_cast<const uint4 *>(arow + col0 + 16 + 8 * j));
           }
           if (has_acc) tmem_ld_wait();
-          if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0);
+          if (valid && col0 < p.N) epilogue_chunk(p, v, av, orow, orow2, col0, rscale, &dpacc);
           av[0] = avn[0];
           av[1] = avn[1];
         }
+        if (p.dp_part && valid) p.dp_part[row * p.dp_parts + (tl.n0 / TN) * 2 + ew / 4] = dpacc;
         if (has_acc) {
           tc_fence_before();
           __syncwarp();
@@ -888,7 +895,8 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
                     const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout, int trans,
                     int epi, int act, void *out, void *out2, const void *aux, const float *pw, float *yacc,
                     int combine_cols, cudaStream_t st, const uint64_t *peer_out = nullptr,
-                    const int32_t *row_src = nullptr, const int32_t *row_slot = nullptr) {
+                    const int32_t *row_src = nullptr, const int32_t *row_slot = nullptr,
+                    float *dp_part = nullptr, int dp_parts = 0) {
   const int64_t d_in = trans ? w_cols : w_rows;
   const int64_t d_out = trans ? w_rows : w_cols;
   CUtensorMap ta, tb;
@@ -916,8 +924,10 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.epi = epi;
   p.act = act;
   p.out = (__nv_bfloat16 *)out;
-  p.out2 = (epi == SMOE_EPI_ACT) ? (__nv_bfloat16 *)out2 : nullptr;
-  p.aux = (epi == SMOE_EPI_ACT_GRAD) ? (const __nv_bfloat16 *)aux : nullptr;
+  p.out2 = (epi == SMOE_EPI_ACT || epi == SMOE_EPI_ACT_SCALED) ? (__nv_bfloat16 *)out2 : nullptr;
+  p.aux = (epi == SMOE_EPI_ACT_GRAD || epi == SMOE_EPI_ACT_GRAD_SCALED) ? (const __nv_bfloat16 *)aux : nullptr;
+  p.dp_part = dp_part;
+  p.dp_parts = dp_parts;
   p.x = (const __nv_bfloat16 *)x;
   p.pw = pw;
   p.yacc = yacc;
@@ -950,6 +960,15 @@ int scatter2scatter(const void *x, int64_t x_rows, const void *w, int E, int64_t
                     int epi, int act, void *out, void *out2, const void *aux, cudaStream_t st) {
   return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi, act, out, out2,
                   aux, nullptr, nullptr, 1, st);
+}
+
+// Routing-weight-scaled epilogues (SMOE_EPI_ACT_SCALED / SMOE_EPI_ACT_GRAD_SCALED).
+int scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                           const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout,
+                           int trans, int epi, int act, const float *row_scale, void *out, void *out2,
+                           const void *aux, float *dp_part, int dp_parts, cudaStream_t st) {
+  return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi, act, out, out2,
+                  aux, row_scale, nullptr, 1, st, nullptr, nullptr, nullptr, dp_part, dp_parts);
 }
 
 // Grouped-input GEMM whose epilogue stores output row i straight into row

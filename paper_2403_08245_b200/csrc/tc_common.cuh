@@ -46,7 +46,16 @@ struct Params {
   const uint64_t *peer_out;
   const int32_t *row_src;
   const int32_t *row_slot;
+  float *dp_part;          // EPI_ACT_GRAD_SCALED: [M, dp_parts] partial dot products
+  int dp_parts;
 };
+
+__device__ __forceinline__ bool epi_scaled(int epi) {
+  return epi == SMOE_EPI_ACT_SCALED || epi == SMOE_EPI_ACT_GRAD_SCALED;
+}
+__device__ __forceinline__ bool epi_act_grad(int epi) {
+  return epi == SMOE_EPI_ACT_GRAD || epi == SMOE_EPI_ACT_GRAD_SCALED;
+}
 
 // ---- PTX wrappers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -322,20 +331,35 @@ __device__ __forceinline__ void zero_k_tail(uint8_t *base, int boxes, int valid,
   zero_k_rows(base, boxes, valid, 64, lane);
 }
 
-// Epilogue for one 16-column chunk of one accumulator row (fp32 in v[]).
+// Epilogue for one 16-column chunk of one accumulator row (fp32 in v[]);
+// scale / dpacc serve the *_SCALED epilogues (see epilogue_pack32).
 __device__ __forceinline__ void epilogue_chunk(const Params &p, const uint32_t (&v)[16], const uint4 (&av)[2],
-                                               __nv_bfloat16 *orow, __nv_bfloat16 *orow2, int64_t col0) {
+                                               __nv_bfloat16 *orow, __nv_bfloat16 *orow2, int64_t col0,
+                                               float scale = 1.0f, float *dpacc = nullptr) {
   float f[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
   uint32_t o1[8], o2[8];
-  if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_ONLY) {
+  if (p.epi == SMOE_EPI_ACT_GRAD_SCALED) {
+    const __nv_bfloat162 *ah = reinterpret_cast<const __nv_bfloat162 *>(av);
+    float dsum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float h0, g0, h1, g1;
+      act_both_fast(p.act, __bfloat162float(ah[i].x), h0, g0);
+      act_both_fast(p.act, __bfloat162float(ah[i].y), h1, g1);
+      dsum = fmaf(f[2 * i], __bfloat162float(__float2bfloat16_rn(h0)), dsum);
+      dsum = fmaf(f[2 * i + 1], __bfloat162float(__float2bfloat16_rn(h1)), dsum);
+      o1[i] = pack_bf16(scale * f[2 * i] * g0, scale * f[2 * i + 1] * g1);
+    }
+    *dpacc += dsum;
+  } else if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_ONLY || p.epi == SMOE_EPI_ACT_SCALED) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       __nv_bfloat162 pre = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
       o1[i] = *reinterpret_cast<uint32_t *>(&pre);
-      float a0 = act_fwd_fast(p.act, __bfloat162float(pre.x));
-      float a1 = act_fwd_fast(p.act, __bfloat162float(pre.y));
+      float a0 = scale * act_fwd_fast(p.act, __bfloat162float(pre.x));
+      float a1 = scale * act_fwd_fast(p.act, __bfloat162float(pre.y));
       o2[i] = pack_bf16(a0, a1);
     }
     if (p.epi == SMOE_EPI_ACT_ONLY) {
@@ -358,7 +382,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params &p, const uint32_t (
   for (int j = 0; j < 2; ++j) {
     if (col0 + 8 * j >= p.N) break;
     *reinterpret_cast<uint4 *>(orow + col0 + 8 * j) = make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
-    if (p.epi == SMOE_EPI_ACT)
+    if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_SCALED)
       *reinterpret_cast<uint4 *>(orow2 + col0 + 8 * j) = make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
   }
 }
@@ -454,10 +478,27 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 //                     EPI_ACT_ONLY, act(round(acc)); for EPI_ACT_GRAD io holds the
 //                     32 bf16 of h_pre on entry and acc * act'(h_pre) on return;
 //   act_pass = true : act(round(acc)) (EPI_ACT's second output).
+//   EPI_ACT_SCALED's act pass multiplies by the row scale before rounding;
+//   EPI_ACT_GRAD_SCALED returns scale * acc * act'(h_pre) and adds
+//   sum(acc * round(act(h_pre))) to dpacc.
 __device__ __forceinline__ void epilogue_pack32(const Params &p, const uint32_t (&v)[32], uint32_t (&io)[16],
-                                                bool act_pass) {
+                                                bool act_pass, float scale = 1.0f, float *dpacc = nullptr) {
   const bool apply_act = act_pass || p.epi == SMOE_EPI_ACT_ONLY;
-  if (p.epi == SMOE_EPI_ACT_GRAD) {
+  if (p.epi == SMOE_EPI_ACT_GRAD_SCALED) {
+    float dsum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&io[i]);
+      float f0, g0, f1, g1;
+      act_both_fast(p.act, __bfloat162float(a.x), f0, g0);
+      act_both_fast(p.act, __bfloat162float(a.y), f1, g1);
+      const float v0 = __uint_as_float(v[2 * i]), v1 = __uint_as_float(v[2 * i + 1]);
+      dsum = fmaf(v0, __bfloat162float(__float2bfloat16_rn(f0)), dsum);
+      dsum = fmaf(v1, __bfloat162float(__float2bfloat16_rn(f1)), dsum);
+      io[i] = pack_bf16(scale * v0 * g0, scale * v1 * g1);
+    }
+    *dpacc += dsum;
+  } else if (p.epi == SMOE_EPI_ACT_GRAD) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162 *>(&io[i]);
@@ -468,7 +509,8 @@ __device__ __forceinline__ void epilogue_pack32(const Params &p, const uint32_t 
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const __nv_bfloat162 pre = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-      io[i] = pack_bf16(act_fwd_fast(p.act, __bfloat162float(pre.x)), act_fwd_fast(p.act, __bfloat162float(pre.y)));
+      io[i] = pack_bf16(scale * act_fwd_fast(p.act, __bfloat162float(pre.x)),
+                        scale * act_fwd_fast(p.act, __bfloat162float(pre.y)));
     }
   } else {
 #pragma unroll

@@ -409,6 +409,9 @@ int group_xty_scattered(const void *, int64_t, int, int, const void *, int64_t, 
 int scatter2scatter_peer(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
                          const int32_t *, int64_t, int, const uint64_t *, const int32_t *, const int32_t *,
                          cudaStream_t);
+int scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                           const int32_t *, int64_t, int, int, int, int, int, int, const float *, void *, void *,
+                           const void *, float *, int, cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -508,6 +511,17 @@ int tc_scatter2scatter_peer(const void *x, int64_t x_rows, const void *w, int E,
     return fail(SMOE_ENOTSUP, "peer-store GEMM needs the CTA-pair engine, d_in, d_out multiples of 8");
   return tc2::scatter2scatter_peer(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, trans, peer_out, row_src,
                                    row_slot, st);
+}
+
+int tc_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                              const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int gout,
+                              int trans, int epi, int act, const float *row_scale, void *out, void *out2,
+                              const void *aux, float *dp_part, int dp_parts, cudaStream_t st) {
+  const int64_t d_in = trans ? w_cols : w_rows, d_out = trans ? w_rows : w_cols;
+  if (!(tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && tc_supports_s2s(d_in, d_out, x, w, out)))
+    return fail(SMOE_ENOTSUP, "scaled epilogues need the CTA-pair engine, d_in, d_out multiples of 8");
+  return tc2::scatter2scatter_scaled(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi,
+                                     act, row_scale, out, out2, aux, dp_part, dp_parts, st);
 }
 
 // group_xty with scattered (gathered) operands: CTA-pair kernels only.

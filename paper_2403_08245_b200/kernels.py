@@ -348,6 +348,78 @@ def group_xty(
     return out
 
 
+def scatter2scatter_scaled(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    order: GroupedOrder,
+    fan_out: int,
+    layout: LayoutFlag,
+    *,
+    row_scale: torch.Tensor,
+    activation: str,
+    out: torch.Tensor,
+    act_out: torch.Tensor | None = None,
+    act_grad_of: torch.Tensor | None = None,
+    dp_partials: torch.Tensor | None = None,
+    transpose_w: bool = False,
+) -> torch.Tensor:
+    """scatter2scatter with a routing-weight-scaled activation epilogue (bf16, tcgen05).
+
+    act_out given: out = x @ W (pre-activation), act_out = s * act(out);
+    act_grad_of given: out = s * (x @ W) * act'(act_grad_of) and, when
+    dp_partials ([n, dp_parts(d_out)] fp32) is given, the per-row partial dot
+    products sum(acc * act(act_grad_of)) for the combine-weight gradient.
+    s = row_scale[order.o[i]] for grouped row i (row_scale: one float per slot).
+    """
+    if (act_out is None) == (act_grad_of is None):
+        raise ValueError("give exactly one of act_out / act_grad_of")
+    if activation not in _lib.ACTIVATION_IDS:
+        raise ValueError(f"unknown activation {activation!r}; choose from {sorted(_lib.ACTIVATION_IDS)}")
+    if x.dtype != torch.bfloat16:
+        raise ValueError("scaled epilogues run on the bf16 tensor-core engine")
+    num_slots = order.num_slots
+    d_in = w.shape[2] if transpose_w else w.shape[1]
+    d_out = w.shape[1] if transpose_w else w.shape[2]
+    require_dims(x.shape[1] == d_in, "input width vs expert weights", tuple(x.shape), (d_in, d_out))
+    require_dims(tuple(out.shape) == (num_slots, d_out), "out buffer", tuple(out.shape), (num_slots, d_out))
+    require_dims(tuple(row_scale.shape) == (num_slots,), "row scale", tuple(row_scale.shape), (num_slots,))
+    x, w = _cuda(x, "x"), _cuda(w, "w")
+    scale = _cuda(row_scale.to(torch.float32), "row_scale")
+    epi = _lib.EPI_ACT_SCALED if act_out is not None else _lib.EPI_ACT_GRAD_SCALED
+    parts = 0
+    if dp_partials is not None:
+        parts = _lib.load().smoe_dp_parts(d_out)
+        require_dims(tuple(dp_partials.shape) == (num_slots, parts), "dp partials", tuple(dp_partials.shape),
+                     (num_slots, parts))
+    aux = None if act_grad_of is None else _cuda(act_grad_of, "act_grad_of")
+    t0 = _lt.begin()
+    st = _lib.load().smoe_scatter2scatter_scaled(
+        x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], w.shape[1], w.shape[2], order.o.data_ptr(),
+        order.bin_offsets.data_ptr(), num_slots, fan_out, int(layout.grouped_in), int(layout.grouped_out),
+        int(transpose_w), epi, _lib.ACTIVATION_IDS[activation], scale.data_ptr(), out.data_ptr(), _ptr(act_out),
+        _ptr(aux), _ptr(dp_partials), parts, _stream(x))
+    _lt.end(_s2s_label(layout, transpose_w, _lib.EPI_ACT if act_out is not None else _lib.EPI_ACT_GRAD) + " scaled",
+            t0)
+    _lib.check(st, "scatter2scatter_scaled")
+    _credit(order, d_in, d_out)
+    return out
+
+
+def dp_parts(d_out: int) -> int:
+    return int(_lib.load().smoe_dp_parts(d_out))
+
+
+def dp_from_partials(partials: torch.Tensor, order: GroupedOrder, s: int, j: int) -> torch.Tensor:
+    """dp (s, j) float32 from the [n, parts] partial dot products of grouped rows."""
+    dp = torch.empty((s, j), dtype=torch.float32, device=partials.device)
+    t0 = _lt.begin()
+    st = _lib.load().smoe_dp_from_partials(partials.data_ptr(), partials.shape[0], partials.shape[1],
+                                           order.o.data_ptr(), dp.data_ptr(), _stream(partials))
+    _lt.end("dp_from_partials", t0)
+    _lib.check(st, "dp_from_partials")
+    return dp
+
+
 def group_xty_scattered(
     x: torch.Tensor,
     y: torch.Tensor,

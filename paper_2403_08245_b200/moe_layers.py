@@ -22,6 +22,7 @@ form, and the shared K/V projections as library GEMMs.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,7 @@ from . import kernels as K
 from . import parallel_linear as pl
 from .errors import require_dims
 from .kernels import (
+    GROUPED_TO_GROUPED,
     GROUPED_TO_SCATTERED,
     SCATTERED_TO_GROUPED,
     SCATTERED_TO_SCATTERED,
@@ -110,11 +112,45 @@ def init_smoe_mlp_weights(config: SmoeMlpConfig, seed: int, dtype=torch.float32,
 
 
 @dataclass
+class _ScaledState:
+    """Saved tensors of the routing-weight-scaled MLP path (see smoe_mlp_forward)."""
+    x: torch.Tensor
+    w1: torch.Tensor
+    w2: torch.Tensor
+    order: GroupedOrder
+    p: torch.Tensor
+    hp: torch.Tensor        # p[slot] * act(h_pre), grouped (the layer-2 input)
+    y_hat_p: torch.Tensor   # layer-2 output rows p * Y_hat in slot order (storage reused in the backward)
+
+
+@dataclass
 class SmoeMlpContext:
-    hidden_ctx: pl.LinearContext
-    output_ctx: pl.LinearContext
+    hidden_ctx: pl.LinearContext | None
+    output_ctx: pl.LinearContext | None
     h_pre: torch.Tensor
     activation: str
+    scaled: _ScaledState | None = None
+
+
+# The routing weight moves through layer 2: layer 1's epilogue writes
+# p * act(h_pre), so Y = sum over the k slot rows of layer 2's output (an
+# unweighted reduce), and dp comes out of the dH GEMM's epilogue as
+# <dY W2^T, act(h_pre)> = <dY, Y_hat> — no retained Y_hat and no dp pass over
+# it.  SMOE_MLP_SCALED=0 runs the reference's literal sequence instead
+# (moe_layers.py:140-211: combine after layer 2, dp from the retained output).
+_SCALED = os.environ.get("SMOE_MLP_SCALED", "1") != "0"
+
+
+def set_scaled(enabled: bool) -> bool:
+    """Select the routing-weight-scaled MLP path (True) or the literal one; returns the previous value."""
+    global _SCALED
+    prev, _SCALED = _SCALED, bool(enabled)
+    return prev
+
+
+def _scaled_ok(x: torch.Tensor, w1: torch.Tensor, order: GroupedOrder) -> bool:
+    return (_SCALED and x.dtype == torch.bfloat16 and K.get_engine() != "simt" and order.num_experts <= 128
+            and os.environ.get("SMOE_TC_CTAS", "2") != "1" and x.shape[1] % 8 == 0 and w1.shape[2] % 8 == 0)
 
 
 @dataclass
@@ -149,6 +185,21 @@ def smoe_mlp_forward(
     if order.num_slots != x.shape[0] * k:
         raise ValueError(f"order covers {order.num_slots} slots but routing implies {x.shape[0]}*{k}")
     n, de = order.num_slots, w1.shape[2]
+    if training and _scaled_ok(x, w1, order):
+        p_flat = routing.p.reshape(-1).to(torch.float32).contiguous()
+        h_pre = torch.empty((n, de), dtype=x.dtype, device=x.device)
+        hp = torch.empty((n, de), dtype=x.dtype, device=x.device)
+        K.scatter2scatter_scaled(x, w1, order, k, SCATTERED_TO_GROUPED, row_scale=p_flat, activation=activation,
+                                 out=h_pre, act_out=hp)
+        y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_SCATTERED)
+        y = K.fanout_reduce(y_hat_p, k)
+        if ledger:
+            ledger.alloc("mlp.hidden.y", n, de, "forward")
+            ledger.alloc("mlp.h_preactivation", n, de, "backward")
+            ledger.alloc("mlp.output.y_hat", n, w2.shape[2], "backward")
+            ledger.alloc("mlp.output.y", y.shape[0], y.shape[1], "forward")
+        st = _ScaledState(x=x, w1=w1, w2=w2, order=order, p=routing.p, hp=hp, y_hat_p=y_hat_p)
+        return y, SmoeMlpContext(hidden_ctx=None, output_ctx=None, h_pre=h_pre, activation=activation, scaled=st)
     if training:
         h_pre = torch.empty((n, de), dtype=x.dtype, device=x.device)
         h = torch.empty((n, de), dtype=x.dtype, device=x.device)
@@ -180,6 +231,8 @@ def smoe_mlp_backward(ctx: SmoeMlpContext, dy: torch.Tensor, *, tile: TileConfig
     pre-combine output's storage takes the hidden transform's grouped input.
     No new T*k-row buffer is allocated.
     """
+    if ctx.scaled is not None:
+        return _scaled_backward(ctx, dy)
     out_ctx = ctx.output_ctx
     hid_ctx = ctx.hidden_ctx
     out_ctx.scratch_grouped_x = out_ctx.x
@@ -189,6 +242,38 @@ def smoe_mlp_backward(ctx: SmoeMlpContext, dy: torch.Tensor, *, tile: TileConfig
     hid_ctx.scratch_grouped_x = out_ctx.y_hat
     g1 = pl.backward(hid_ctx, dh, tile=tile, ledger=ledger, name="mlp.hidden")
     return SmoeMlpGradients(dx=g1.dx, dw1=g1.dw, dw2=g2.dw, dp=g2.dp)
+
+
+def _scaled_backward(ctx: SmoeMlpContext, dy: torch.Tensor) -> SmoeMlpGradients:
+    """Backward of the routing-weight-scaled path; same buffer reuse as the
+    reference (moe_layers.py:198-211): grouped dY and then the grouped input
+    live in the retained output's storage, dH overwrites p * act(h_pre) after
+    dW2 consumed it, the slot input-gradients overwrite the grouped input."""
+    st = ctx.scaled
+    order, k = st.order, st.p.shape[1]
+    t = st.p.shape[0]
+    if tuple(dy.shape) != (t, st.w2.shape[2]):
+        require_dims(False, "dy vs combine output", tuple(dy.shape), (t, st.w2.shape[2]))
+    dy = dy.contiguous()
+    p_flat = st.p.reshape(-1).to(torch.float32).contiguous()
+    de = st.w1.shape[2]
+    dyg = K.group(dy, order, fan_out=k, out=st.y_hat_p)
+    dw2 = K.group_xty(st.hp, dyg, order)
+    parts = torch.empty((order.num_slots, K.dp_parts(de)), dtype=torch.float32, device=dy.device)
+    dh = K.scatter2scatter_scaled(dyg, st.w2, order, 1, GROUPED_TO_GROUPED, row_scale=p_flat,
+                                  activation=ctx.activation, out=st.hp, act_grad_of=ctx.h_pre,
+                                  dp_partials=parts, transpose_w=True)
+    dp = K.dp_from_partials(parts, order, t, k)
+    if pl._gather_ok(de, st.x) and order.num_experts <= 128:
+        dw1 = K.group_xty_scattered(st.x, dh, order, x_fan_out=k, y_grouped=True)
+        slot_out = dyg
+    else:
+        xbar = K.group(st.x, order, fan_out=k, out=dyg)
+        dw1 = K.group_xty(xbar, dh, order)
+        slot_out = xbar
+    slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_SCATTERED, transpose_w=True, out=slot_out)
+    dx = K.fanout_reduce(slot, k)
+    return SmoeMlpGradients(dx=dx, dw1=dw1, dw2=dw2, dp=dp)
 
 
 class _SmoeMlpFunction(torch.autograd.Function):

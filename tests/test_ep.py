@@ -117,8 +117,12 @@ def test_ep_world1_nccl_bit_identical_to_single_gpu():
         w2 = ((torch.rand(e, de, d, device="cuda", generator=g) * 2 - 1) / 22).bfloat16()
         routing = sm.topk_select(torch.softmax(torch.randn(t, e, device="cuda", generator=g), 1), k)
         order = sm.compute_grouped_order(routing)
-        y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
-        gr = sm.smoe_mlp_backward(c, dy)
+        prev = sm.moe_layers.set_scaled(False)   # EP combines at the source, like the literal path
+        try:
+            y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+            gr = sm.smoe_mlp_backward(c, dy)
+        finally:
+            sm.moe_layers.set_scaled(prev)
         ep = ExpertParallelSmoeMlp(w1, w2, e)
         y, ctx = ep.forward(x, routing)
         ge = ep.backward(ctx, dy)

@@ -84,6 +84,7 @@ def _worker(rank, world, port, q, fused="1", shape="c1"):
         routing = sm.topk_select(torch.softmax(logits, 1), K)
         # single-process reference on the concatenated batch
         order = sm.compute_grouped_order(routing)
+        sm.moe_layers.set_scaled(False)   # EP combines at the source, like the literal path
         y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
         g_ref = sm.smoe_mlp_backward(c, dy)
         sl = slice(rank * T_LOCAL, (rank + 1) * T_LOCAL)

@@ -80,17 +80,23 @@ def test_c0_fp32_check_mode():
         assert rel_err(got, w_) <= 1e-4, (name, rel_err(got, w_))
 
 
-@pytest.mark.parametrize("engine", ["simt", "auto"])
-def test_c0_bf16(engine):
+@pytest.mark.parametrize("engine,scaled", [("simt", True), ("auto", True), ("auto", False)])
+def test_c0_bf16(engine, scaled):
+    """scaled: the routing weight moved through layer 2 (dp from the dH epilogue);
+    False: the reference's literal sequence (combine, dp from the retained output)."""
     x, w1, w2, idx, p, dy = _c0(True)
     want_y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, 8)
     want = orc.smoe_mlp_backward(x, w1, w2, p, st, dy)
     sm.set_engine(engine)
+    prev = sm.moe_layers.set_scaled(scaled)
     try:
         y, ctx = _run(x, w1, w2, idx, p, 8, "gelu", torch.bfloat16)
+        if engine == "auto":
+            assert (ctx.scaled is not None) == scaled
         gr = sm.smoe_mlp_backward(ctx, t(dy, torch.bfloat16))
     finally:
         sm.set_engine("auto")
+        sm.moe_layers.set_scaled(prev)
     assert rel_err(y, want_y) <= 2e-2
     for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2, gr.dp), want, ("dx", "dw1", "dw2", "dp")):
         assert rel_err(got, w_) <= 2e-2, (name, rel_err(got, w_))
@@ -179,3 +185,33 @@ def test_train_equals_infer_and_relabel_invariance():
     y2, _ = _run(g[pre + "x"], g[pre + "w1"][inv], g[pre + "w2"][inv], perm[g[pre + "idx"]], g[pre + "p"], 4,
                  "gelu", torch.float32)
     np.testing.assert_allclose(np_of(y2), np_of(y), rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("act", ["gelu", "silu", "relu"])
+@pytest.mark.parametrize("flavor", ["gate", "skewed"])
+def test_scaled_path_matches_literal_path(act, flavor):
+    """The routing-weight-scaled MLP (p through layer 2, dp from the dH epilogue)
+    against the literal sequence, bf16, ragged bins and partial tiles."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    tokens, d, de, e, k = 1000, 136, 264, 6, 2
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / de ** 0.5).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    logits = torch.randn(tokens, e, device="cuda", generator=g)
+    if flavor == "skewed":
+        logits[:, 0] += 6.0
+    routing = sm.topk_select(torch.softmax(logits, 1), k)
+    order = sm.compute_grouped_order(routing)
+    out = {}
+    for scaled in (True, False):
+        prev = sm.moe_layers.set_scaled(scaled)
+        try:
+            y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order, activation=act)
+            assert (ctx.scaled is not None) == scaled
+            gr = sm.smoe_mlp_backward(ctx, dy)
+        finally:
+            sm.moe_layers.set_scaled(prev)
+        out[scaled] = (y, gr.dx, gr.dw1, gr.dw2, gr.dp)
+    for name, a, b in zip(("y", "dx", "dw1", "dw2", "dp"), out[True], out[False]):
+        assert rel_err(a, np_of(b)) <= 1e-2, (name, rel_err(a, np_of(b)))
