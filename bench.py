@@ -336,7 +336,9 @@ def run_ours(args, rank, world, local_rank):
     kernels = {lab: {"launches_per_step": d["launches"] / args.steps, "ms_per_launch": d["ms_per_launch"],
                      "share_of_step": d["ms_total"] / args.steps / ms}
                for lab, d in per_kernel.items()}
-    L1_LABEL = "scatter2scatter S->G +act(pre,post)"
+    # the layer-1 GEMM's label (the routing-weight-scaled MLP path appends " scaled")
+    L1_LABEL = next((lab for lab in kernels if lab.startswith("scatter2scatter S->G +act(pre,post)")),
+                    "scatter2scatter S->G +act(pre,post)")
 
     # ---- roofline: dominant kernel (layer-1 forward grouped GEMM) ----
     # achieved = its algorithmic FLOPs / its mean launch duration inside the
