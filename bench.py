@@ -14,11 +14,13 @@ value  : tokens/s with inputs resident in HBM (device time, CUDA events).
 e2e    : the same step through the public API from pinned HOST buffers:
          X, dY, expert ids and p copied H2D, dX and dp copied D2H, inside the
          timed region.
-roofline: the dominant kernel (the layer-1 forward grouped GEMM): its mean
-         launch duration inside the timed steps (CUDA events around each
-         launch on its stream, launch_timer.py); algorithmic FLOPs =
-         2*T*k*d*d_e.  `kernels` lists every library call's per-launch time and
-         share of the step from the same events.
+roofline: the dominant kernel (the GEMM with the largest share of the step,
+         the grouped-K weight-gradient GEMM at C1/C2): its mean launch
+         duration inside the timed steps (CUDA events around each launch on
+         its stream, launch_timer.py); algorithmic FLOPs = 2*T*k*d*d_e.
+         `roofline_gather` reports the layer-1 gather GEMM the same way.
+         `kernels` lists every library call's per-launch time and share of
+         the step from the same events.
 cpu_baseline: the CPU oracle (NumPy restatement of the reference, oracle/)
          on a bounded sample (T=128 at C1 dims), rank 0 at N=1 only.
 --impl reference: the same metric from the oracle port on the host CPU.
@@ -370,23 +372,37 @@ def run_ours(args, rank, world, local_rank):
     ms_l1_alone = e0.elapsed_time(e1) / reps
     l1_flops = 2.0 * n * d * de
     ms_l1 = kernels[L1_LABEL]["ms_per_launch"] if (world == 1 and L1_LABEL in kernels) else ms_l1_alone
-    achieved = l1_flops / (ms_l1 / 1e3) / 1e12
-    traffic = None
+    traffic_db = {}
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get(f"{args.config}:{sm.get_engine()}:l1_fwd")
+            traffic_db = json.loads(tfile.read_text())
         except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "kernel": "scatter2scatter S->G layer-1 fwd (gather + grouped GEMM + fused GELU epilogue)",
+            traffic_db = {}
+
+    def roof(label, ms_launch, desc, timed):
+        achieved = l1_flops / (ms_launch / 1e3) / 1e12     # every GEMM of the step is 2*n*d*d_e FLOP
+        return {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"],
+                "traffic": traffic_db.get(f"{args.config}:{label}"),
+                "kernel": desc, "label": label,
                 "algorithmic": f"2*T*k*d_model*d_expert = {l1_flops:.4g} FLOP per launch",
-                "ms_per_launch": ms_l1, "ms_per_launch_alone": ms_l1_alone,
-                "share_of_step": kernels.get(L1_LABEL, {}).get("share_of_step"),
-                "timed": "inside the timed steps (CUDA events around each launch on its stream)" if world == 1
-                         else "alone (10 back-to-back launches)",
-                "peak_kind": f"{peak_kind} burst"}
+                "ms_per_launch": ms_launch, "share_of_step": kernels.get(label, {}).get("share_of_step"),
+                "timed": timed, "peak_kind": f"{peak_kind} burst"}
+
+    in_step = "inside the timed steps (CUDA events around each launch on its stream)"
+    gather_roof = roof(L1_LABEL, ms_l1, "scatter2scatter S->G layer-1 fwd (cp.async row gather + grouped GEMM + "
+                       "fused GELU epilogue)", in_step if world == 1 else "alone (10 back-to-back launches)")
+    gather_roof["ms_per_launch_alone"] = ms_l1_alone
+    gemms = {lab: v for lab, v in kernels.items() if lab.startswith(("scatter2scatter", "group_xty"))}
+    if world == 1 and gemms:
+        # the dominant kernel = the GEMM family with the largest share of the step
+        dom = max(gemms, key=lambda lab: gemms[lab]["share_of_step"])
+        dom_desc = ("group_xty: grouped-K tcgen05 GEMM (dW = Xg^T Yg per expert bin; 2 launches per step)"
+                    if dom.startswith("group_xty") else f"{dom} (tcgen05 grouped GEMM)")
+        roofline = roof(dom, gemms[dom]["ms_per_launch"], dom_desc, in_step)
+    else:
+        roofline = gather_roof
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -416,6 +432,7 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
             "gpu_launches": launches,
             "roofline": roofline,
+            "roofline_gather": gather_roof,
             "kernels": kernels,
             "cpu_baseline": cpu_baseline,
             "clocks": clocks,

@@ -58,6 +58,16 @@ for _ in range(3):
         torch.matmul(xg, w[0])
     elif which == "xtysg":  # dW1 with X gathered by slot (no grouped copy)
         sm.kernels.group_xty_scattered(x, h, order, x_fan_out=k, y_grouped=True)
+    elif which == "l1s":  # layer 1 on the routing-weight-scaled MLP path (bench's kernel)
+        pf = routing.p.reshape(-1).float().contiguous()
+        sm.kernels.scatter2scatter_scaled(x, w, order, k, sm.SCATTERED_TO_GROUPED, row_scale=pf, activation="gelu",
+                                          out=h, act_out=h2)
+    elif which == "dhs":  # dH with p scale + dp partials (bench's kernel)
+        pf = routing.p.reshape(-1).float().contiguous()
+        parts = torch.empty((n, sm.kernels.dp_parts(de)), dtype=torch.float32, device=dev)
+        sm.kernels.scatter2scatter_scaled(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, row_scale=pf,
+                                          activation="gelu", out=h2, act_grad_of=h, dp_partials=parts,
+                                          transpose_w=True)
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()
