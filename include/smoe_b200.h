@@ -120,6 +120,13 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
                          int32_t dtype, int32_t epilogue, int32_t activation, void *out,
                          void *out2, const void *aux, int32_t engine, void *stream);
 
+/* group (kernels.py:289-326) visited by source row: out[inverse[s]] =
+ * x[s / fan_out] * (weights ? weights[s] : 1) for every slot s (fan_out <= 16;
+ * inverse = the grouped position of each slot, from smoe_route_sort).  Each
+ * source row is read once instead of once per expert bin. */
+int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
+                   const float *weights, int32_t dtype, void *out, void *stream);
+
 /* ---------------------------------------------------------------------------
  * group_xty (kernels.py:329-361): dw[e] = xg[bin e]^T @ yg[bin e]; empty bin -> 0.
  *   xg [n, d_in], yg [n, d_out] (grouped order), dw [E, d_in, d_out]

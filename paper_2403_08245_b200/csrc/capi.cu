@@ -32,6 +32,7 @@ int combine(const void *, const float *, int64_t, int, int64_t, int, void *, cud
 int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, float *, cudaStream_t);
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
+int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const float *, int, void *, cudaStream_t);
 int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
                               const int32_t *, int64_t, int, int, int, int, int, int, const float *, void *, void *,
                               const void *, float *, int, cudaStream_t);
@@ -189,6 +190,15 @@ int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, i
   if (n == 0) return SMOE_OK;
   REQUIRE(x && order && out, SMOE_EINVAL, "group: null pointer");
   return group(x, d, order, n, fan_out, weights, dtype, out, S(stream));
+}
+
+int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
+                   const float *weights, int32_t dtype, void *out, void *stream) {
+  REQUIRE(fan_out >= 1 && fan_out <= 16, SMOE_EINVAL, "group_inv: fan_out must be in [1, 16]");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (x_rows == 0) return SMOE_OK;
+  REQUIRE(x && inverse && out, SMOE_EINVAL, "group_inv: null pointer");
+  return group_inv(x, x_rows, d, inverse, fan_out, weights, dtype, out, S(stream));
 }
 
 int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_cols, int64_t d,

@@ -65,6 +65,50 @@ __global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict_
   }
 }
 
+// ---- group, token-major (fan-out > 1) ---------------------------------------
+// Same result as group_kernel, visited by source row: one warp loads x[t] once
+// and writes it (times w[s]) to the k grouped positions inv[s], s = t*F + j.
+// group_kernel's grouped-order visit re-reads each source row once per bin
+// (k times, from DRAM when x exceeds L2); this reads it once.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restrict__ x, int64_t d,
+                                                                const int32_t *__restrict__ inv, int64_t t_rows,
+                                                                int fan_out, const float *__restrict__ weights,
+                                                                T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (t >= t_rows) return;
+  const T *src = x + t * d;
+  constexpr int MAXF = 16;
+  int64_t dst[MAXF];
+  float wgt[MAXF];
+  const int F = fan_out < MAXF ? fan_out : MAXF;
+  for (int j = 0; j < F; ++j) {
+    const int64_t s = t * fan_out + j;
+    dst[j] = (int64_t)inv[s] * d;
+    wgt[j] = weights ? weights[s] : 1.0f;
+  }
+  if (VEC) {
+    constexpr int N = Vec<T>::N;
+    for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+      const Vec<T> v = ldv(src + c);
+      for (int j = 0; j < F; ++j) {
+        Vec<T> o = v;
+        if (weights) {
+#pragma unroll
+          for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(Num<T>::to_f(v.v[q]) * wgt[j]);
+        }
+        stv(out + dst[j] + c, o);
+      }
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) {
+      const T v = src[c];
+      for (int j = 0; j < F; ++j) out[dst[j] + c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt[j]) : v;
+    }
+  }
+}
+
 // ---- combine ---------------------------------------------------------------
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,
@@ -199,6 +243,29 @@ int group(const void *x, int64_t d, const int32_t *order, int64_t n, int fan_out
       group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
   }
   return check_launch("group");
+}
+
+int group_inv(const void *x, int64_t t_rows, int64_t d, const int32_t *inv, int fan_out, const float *w, int dtype,
+              void *out, cudaStream_t st) {
+  if (t_rows == 0 || d == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16) {
+    using T = __nv_bfloat16;
+    if (vec_ok(x, d, 2) && vec_ok(out, d, 2))
+      group_inv_kernel<T, true><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out, w,
+                                                                             (T *)out);
+    else
+      group_inv_kernel<T, false><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
+                                                                              w, (T *)out);
+  } else {
+    using T = float;
+    if (vec_ok(x, d, 4) && vec_ok(out, d, 4))
+      group_inv_kernel<T, true><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out, w,
+                                                                             (T *)out);
+    else
+      group_inv_kernel<T, false><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
+                                                                              w, (T *)out);
+  }
+  return check_launch("group_inv");
 }
 
 int combine(const void *y_hat, const float *p, int64_t S, int J, int64_t d, int dtype, void *y,

@@ -71,6 +71,9 @@ _mac_lock = threading.Lock()
 _mac_count = 0
 _fault_inject = False
 _engine = os.environ.get("SMOE_ENGINE", "auto")
+# group() with fan-out > 1 walks source rows (smoe_group_inv) instead of grouped
+# positions; SMOE_GROUP_BY_TOKEN=0 keeps the grouped-order walk (A/B)
+_GROUP_BY_TOKEN = os.environ.get("SMOE_GROUP_BY_TOKEN", "1") != "0"
 
 
 def reset_mac_count() -> None:
@@ -309,8 +312,13 @@ def group(
         if out.dtype != x.dtype:
             raise ValueError(f"out dtype {out.dtype} does not match input dtype {x.dtype}")
     t0 = _lt.begin()
-    st = _lib.load().smoe_group(x.data_ptr(), x.shape[0], x.shape[1], order.o.data_ptr(), num_slots,
-                                fan_out, _ptr(weights), _dtype_id(x), out.data_ptr(), _stream(x))
+    if _GROUP_BY_TOKEN and 1 < fan_out <= 16 and order.inv is not None:
+        # visited by source row: each x row read once, written to its k grouped positions
+        st = _lib.load().smoe_group_inv(x.data_ptr(), x.shape[0], x.shape[1], order.inv.data_ptr(), fan_out,
+                                        _ptr(weights), _dtype_id(x), out.data_ptr(), _stream(x))
+    else:
+        st = _lib.load().smoe_group(x.data_ptr(), x.shape[0], x.shape[1], order.o.data_ptr(), num_slots,
+                                    fan_out, _ptr(weights), _dtype_id(x), out.data_ptr(), _stream(x))
     _lt.end("group", t0)
     _lib.check(st, "group")
     return out

@@ -254,3 +254,24 @@ def test_group_xty_scattered_matches_group_then_xty(engine, flavor, grouped):
             assert rel_err(got, ref) <= 1e-5
         if flavor == "skip_one":
             assert float(got[e - 1].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 8])
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_group_token_major_equals_grouped_walk(k, weighted, dtype):
+    """group() walking source rows (smoe_group_inv) == walking grouped positions."""
+    rng = np.random.default_rng(k * 7 + weighted)
+    tokens, e, d = 777, 9, 264
+    idx = np.stack([rng.permutation(e)[:k] for _ in range(tokens)])
+    order = order_of(idx, e)
+    x = t(rng.uniform(-1, 1, (tokens, d)).astype(np.float32), dtype)
+    w = t(rng.uniform(0, 1, tokens * k).astype(np.float32)) if weighted else None
+    got = sm.group(x, order, weights=w, fan_out=k)
+    prev = sm.kernels._GROUP_BY_TOKEN
+    sm.kernels._GROUP_BY_TOKEN = False
+    try:
+        want = sm.group(x, order, weights=w, fan_out=k)
+    finally:
+        sm.kernels._GROUP_BY_TOKEN = prev
+    assert torch.equal(got, want)
