@@ -387,12 +387,15 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       // ===================== relay (peer CTA, gather mode): own stage landed -> leader =====================
       int stage = 0;
       uint32_t phase = 0;
+      long long r_start = clock64(), r_wait = 0;  // p.timing == 2: relay busy/wait cycles
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
         const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
+          long long w0 = p.timing ? clock64() : 0;
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          if (p.timing) r_wait += clock64() - w0;
           if (KGATHER && !(GA && GB)) {
             // grouped-K bin tail: the TMA operand's rows past the bin belong to
             // the next expert; zero them up to the K16 step the leader issues
@@ -409,6 +412,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (p.timing == 2 && lane == 0 && cluster_id < 4)
+        printf("tc2 relay cluster %d: total %lld cyc, waiting on own stage %lld (%.1f%%)\n", (int)cluster_id,
+               clock64() - r_start, r_wait, 100.0 * r_wait / (clock64() - r_start));
     }
   } else if (warp < EPI_WARPS) {
     if constexpr (STAGED) {
