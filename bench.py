@@ -282,7 +282,8 @@ def run_ours(args, rank, world, local_rank):
     # Double-buffered input pipeline, as a training loop would run it: step i+1's
     # H2D copies and step i's D2H copies run on a copy stream while step i
     # computes.  Every step's copies are inside the timed region.
-    cs = torch.cuda.Stream(device=dev)
+    cs = torch.cuda.Stream(device=dev)        # H2D of the next step's inputs
+    cs_out = torch.cuda.Stream(device=dev)    # D2H of this step's results (its own copy engine)
     dbufs = [dict(x=torch.empty_like(x), dy=torch.empty_like(dy), ids=torch.empty_like(routing.expert_idx),
                   p=torch.empty_like(routing.p)) for _ in range(2)]
     ev_in = [torch.cuda.Event() for _ in range(2)]      # forward inputs (ids, p, X) landed
@@ -314,13 +315,14 @@ def run_ours(args, rank, world, local_rank):
                                   validate=False)
             _, grads = step(b["x"], b["dy"], rt, dy_ready=lambda: st.wait_event(ev_dy[slot]))
             ev_done[slot].record(st)
-            with torch.cuda.stream(cs):
-                cs.wait_event(ev_done[slot])
+            with torch.cuda.stream(cs_out):
+                cs_out.wait_event(ev_done[slot])
                 hdx.copy_(grads.dx, non_blocking=True)
                 hdp.copy_(grads.dp, non_blocking=True)
-                grads.dx.record_stream(cs)
-                grads.dp.record_stream(cs)
+                grads.dx.record_stream(cs_out)
+                grads.dp.record_stream(cs_out)
         st.wait_stream(cs)
+        st.wait_stream(cs_out)
 
     e2e_run(max(2, args.warmup))
     torch.cuda.synchronize()
