@@ -215,3 +215,39 @@ def test_scaled_path_matches_literal_path(act, flavor):
         out[scaled] = (y, gr.dx, gr.dw1, gr.dw2, gr.dp)
     for name, a, b in zip(("y", "dx", "dw1", "dw2", "dp"), out[True], out[False]):
         assert rel_err(a, np_of(b)) <= 1e-2, (name, rel_err(a, np_of(b)))
+
+
+@pytest.mark.parametrize("tokens,d,de,e,k,flavor", [
+    (1, 64, 128, 1, 1, "gate"),          # one token, one expert
+    (3, 64, 64, 4, 2, "gate"),           # fewer rows than one tile
+    (513, 128, 192, 16, 4, "all_to_one"),  # every token to experts 0..3, 12 empty bins
+    (2048, 256, 256, 128, 8, "gate"),    # 128 experts (largest on the CTA-pair engine)
+])
+def test_scaled_mlp_edge_cases_vs_oracle(tokens, d, de, e, k, flavor):
+    rng = np.random.default_rng(tokens + e)
+    x = bf16_round(rng.uniform(-1, 1, (tokens, d)).astype(np.float32))
+    w1 = bf16_round((rng.uniform(-1, 1, (e, d, de)) / np.sqrt(d)).astype(np.float32))
+    w2 = bf16_round((rng.uniform(-1, 1, (e, de, d)) / np.sqrt(de)).astype(np.float32))
+    dy = bf16_round(rng.uniform(-1, 1, (tokens, d)).astype(np.float32))
+    if flavor == "all_to_one":
+        idx = np.tile(np.arange(k), (tokens, 1))
+    else:
+        idx = np.stack([rng.permutation(e)[:k] for _ in range(tokens)])
+    p = rng.uniform(0.05, 1.0, (tokens, k)).astype(np.float32)
+    p /= p.sum(1, keepdims=True)
+    want_y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, e)
+    want = orc.smoe_mlp_backward(x, w1, w2, p, st, dy)
+    y, ctx = _run(x, w1, w2, idx, p, e, "gelu", torch.bfloat16)
+    assert ctx.scaled is not None
+    gr = sm.smoe_mlp_backward(ctx, t(dy, torch.bfloat16))
+    assert rel_err(y, want_y) <= 2e-2
+    for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2), want[:3], ("dx", "dw1", "dw2")):
+        assert rel_err(got, w_) <= 2e-2, (name, rel_err(got, w_))
+    # dp entries are single dot products: with few tokens the Frobenius norm is
+    # dominated by cancelling ones, so bound each by its absolute dot product
+    absdot = np.abs(dy).astype(np.float64)[:, None, :] * np.abs(st["y_hat"]).reshape(tokens, k, d)
+    absdot = absdot.sum(-1)
+    err = np.abs(np_of(gr.dp).astype(np.float64) - want[3])
+    assert np.all(err <= 2e-2 * absdot + 1e-6), float((err / np.maximum(absdot, 1e-30)).max())
+    if tokens >= 64:
+        assert rel_err(gr.dp, want[3]) <= 2e-2
