@@ -251,3 +251,36 @@ def test_scaled_mlp_edge_cases_vs_oracle(tokens, d, de, e, k, flavor):
     assert np.all(err <= 2e-2 * absdot + 1e-6), float((err / np.maximum(absdot, 1e-30)).max())
     if tokens >= 64:
         assert rel_err(gr.dp, want[3]) <= 2e-2
+
+
+def test_training_step_cuda_graph_capture_bit_identical():
+    """The whole step (routing sort, forward, backward) captures into one CUDA
+    graph (no host syncs, no allocations inside the library) and replays
+    bit-identically to eager execution."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    tokens, d, de, e, k = 2048, 256, 512, 8, 2
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / de ** 0.5).to(torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+
+    def step():
+        order = sm.compute_grouped_order(routing)
+        y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+        return y, sm.smoe_mlp_backward(ctx, dy)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        y_g, gr_g = step()
+    y_e, gr_e = step()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_g, y_e)
+    for a, b in ((gr_g.dx, gr_e.dx), (gr_g.dw1, gr_e.dw1), (gr_g.dw2, gr_e.dw2), (gr_g.dp, gr_e.dp)):
+        assert torch.equal(a, b)
