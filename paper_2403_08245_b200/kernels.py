@@ -74,6 +74,9 @@ _engine = os.environ.get("SMOE_ENGINE", "auto")
 # group() with fan-out > 1 walks source rows (smoe_group_inv) instead of grouped
 # positions; SMOE_GROUP_BY_TOKEN=0 keeps the grouped-order walk (A/B)
 _GROUP_BY_TOKEN = os.environ.get("SMOE_GROUP_BY_TOKEN", "1") != "0"
+# scatter_combine: "auto" fuses the combine into the GEMM epilogue for k <= 2
+# (bit-reproducible, no T*k buffer) and runs GEMM + combine for k > 2; "1"/"0" force
+_COMBINE_FUSED = os.environ.get("SMOE_COMBINE_FUSED", "auto")
 
 
 def reset_mac_count() -> None:
@@ -274,6 +277,15 @@ def scatter_combine(
     x, w = _cuda(x, "x"), _cuda(w, "w")
     p32 = _cuda(p_flat.to(torch.float32), "p_flat")
     rows = num_slots // combine_cols
+    if (x.dtype == torch.bfloat16 and combine_cols > 2 and _COMBINE_FUSED != "1"
+            and (engine or _engine) != "simt") or _COMBINE_FUSED == "0":
+        # k > 2: the fused epilogue's k fp32 additions per token land in completion
+        # order (not bit-reproducible) and its L2 reductions cost more than a
+        # scattered-output GEMM + the token-major combine (C2 layer 2: 4.13 vs
+        # 3.06 + 0.48 ms), so take that route; the n-row buffer it needs is the
+        # memory the fused form saves.
+        y_hat = scatter2scatter(x, w, order, fan_out, LayoutFlag(grouped_in, False), engine=engine)
+        return combine(p32.view(rows, combine_cols), y_hat)
     acc = torch.empty((rows, d_out), dtype=torch.float32, device=x.device)
     y = acc if x.dtype == torch.float32 else torch.empty((rows, d_out), dtype=x.dtype, device=x.device)
     t0 = _lt.begin()

@@ -194,10 +194,19 @@ def test_scatter_combine_bf16_tcgen05(grouped_in, flavor):
         ys = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
                                 t(p.reshape(-1)), k, grouped_in, engine="simt")
         assert rel_err(y, np_of(ys)) <= 1e-2
-        if k <= 2:  # two fp32 additions into a zeroed row commute: bit-reproducible
-            y2 = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
-                                    t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
-            assert torch.equal(y, y2)
+        # k <= 2: two fp32 additions into a zeroed row commute; k > 2 runs GEMM + combine
+        y2 = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+        assert torch.equal(y, y2)
+        if k > 2:  # the fused epilogue forced at k > 2 (reductions in completion order)
+            prev = sm.kernels._COMBINE_FUSED
+            sm.kernels._COMBINE_FUSED = "1"
+            try:
+                yf = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                        t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+            finally:
+                sm.kernels._COMBINE_FUSED = prev
+            assert rel_err(yf, want) <= 2e-2
 
 
 def test_inference_mlp_uses_tcgen05_combine():
