@@ -122,9 +122,9 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
     REQUIRE(x_rows * fan_out == n, SMOE_EINVAL,
             "scattered input rows (" + std::to_string(x_rows) + ") * fan_out (" + std::to_string(fan_out) +
                 ") must equal T*k (" + std::to_string(n) + ")");
+  if (n == 0) return SMOE_OK;  // empty tensors may carry null pointers
   REQUIRE(epilogue != SMOE_EPI_ACT || out2, SMOE_EINVAL, "EPI_ACT needs out2");
   REQUIRE(epilogue != SMOE_EPI_ACT_GRAD || aux, SMOE_EINVAL, "EPI_ACT_GRAD needs aux");
-  if (n == 0) return SMOE_OK;
   REQUIRE(x && w && order && expert_offsets && out, SMOE_EINVAL, "scatter2scatter: null pointer");
   const int64_t d_in = transpose_w ? w_cols : w_rows, d_out = transpose_w ? w_rows : w_cols;
   bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
@@ -243,11 +243,11 @@ int smoe_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, in
     REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");
   else
     REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
-  REQUIRE(epilogue != SMOE_EPI_ACT_SCALED || out2, SMOE_EINVAL, "EPI_ACT_SCALED needs out2");
-  REQUIRE(epilogue != SMOE_EPI_ACT_GRAD_SCALED || aux, SMOE_EINVAL, "EPI_ACT_GRAD_SCALED needs aux");
   const int64_t d_out = transpose_w ? w_rows : w_cols;
   REQUIRE(!dp_part || dp_parts == smoe_dp_parts(d_out), SMOE_EINVAL, "dp_parts must be smoe_dp_parts(d_out)");
-  if (n == 0) return SMOE_OK;
+  if (n == 0) return SMOE_OK;  // empty tensors may carry null pointers
+  REQUIRE(epilogue != SMOE_EPI_ACT_SCALED || out2, SMOE_EINVAL, "EPI_ACT_SCALED needs out2");
+  REQUIRE(epilogue != SMOE_EPI_ACT_GRAD_SCALED || aux, SMOE_EINVAL, "EPI_ACT_GRAD_SCALED needs aux");
   REQUIRE(x && w && order && expert_offsets && out && row_scale, SMOE_EINVAL, "scatter2scatter_scaled: null pointer");
   REQUIRE(tc_available(), SMOE_ENOTSUP, "scaled epilogues run on the tcgen05 engine");
   return tc_scatter2scatter_scaled(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
@@ -286,8 +286,9 @@ int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t n
     REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");
   else
     REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
+  if (n == 0) return SMOE_OK;  // empty tensors may carry null pointers
   REQUIRE(y_accum && y, SMOE_EINVAL, "scatter_combine: null output");
-  if (n == 0 || d_out == 0) return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n,
+  if (d_out == 0) return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n,
                                                         fan_out, p_flat, combine_cols, grouped_in, dtype, y_accum, y,
                                                         S(stream));
   REQUIRE(x && w && order && expert_offsets && p_flat, SMOE_EINVAL, "scatter_combine: null pointer");

@@ -57,7 +57,7 @@ def test_dispatch_layout_matches_local_grouped_order(world, e):
 
 
 T_LOCAL, D, DE = 512, 256, 512
-SHAPES = {"c1": (8, 2), "c4": (64, 8)}     # (E, k): Mixtral-like and the fine-grained EP config
+SHAPES = {"c1": (8, 2), "c4": (64, 8), "starve": (8, 2)}  # (E, k); "starve": every token routed to rank 0's experts
 
 
 def _problem(world, E):
@@ -81,6 +81,8 @@ def _worker(rank, world, port, q, fused="1", shape="c1"):
         from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
         torch.cuda.set_device(0)
         x, dy, w1, w2, logits = (a.cuda() for a in _problem(world, E))
+        if shape == "starve":            # the other ranks' experts receive no rows at all
+            logits[:, : E // world] += 100.0
         routing = sm.topk_select(torch.softmax(logits, 1), K)
         # single-process reference on the concatenated batch
         order = sm.compute_grouped_order(routing)
@@ -114,7 +116,8 @@ def _worker(rank, world, port, q, fused="1", shape="c1"):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,fused,shape", [(2, "1", "c1"), (4, "1", "c1"), (2, "0", "c1"), (4, "1", "c4")])
+@pytest.mark.parametrize("world,fused,shape", [(2, "1", "c1"), (4, "1", "c1"), (2, "0", "c1"), (4, "1", "c4"),
+                                               (2, "1", "starve")])
 def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     ctx = mp.get_context("spawn")

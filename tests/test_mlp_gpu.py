@@ -284,3 +284,23 @@ def test_training_step_cuda_graph_capture_bit_identical():
     assert torch.equal(y_g, y_e)
     for a, b in ((gr_g.dx, gr_e.dx), (gr_g.dw1, gr_e.dw1), (gr_g.dw2, gr_e.dw2), (gr_g.dp, gr_e.dp)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("training", [True, False])
+def test_zero_tokens(training):
+    """A batch with no tokens (an EP rank that receives nothing): empty outputs, zero dW."""
+    e, d, de, k = 4, 64, 128, 2
+    w1 = torch.zeros((e, d, de), dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros((e, de, d), dtype=torch.bfloat16, device="cuda")
+    x = torch.zeros((0, d), dtype=torch.bfloat16, device="cuda")
+    routing = sm.RoutingResult(expert_idx=torch.zeros((0, k), dtype=torch.int64, device="cuda"),
+                               p=torch.zeros((0, k), dtype=torch.float32, device="cuda"),
+                               gate_full=torch.zeros((0, e), device="cuda"), renormalized=False, validate=False)
+    order = sm.compute_grouped_order(routing, e)
+    y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=training)
+    assert tuple(y.shape) == (0, d)
+    if training:
+        gr = sm.smoe_mlp_backward(ctx, torch.zeros((0, d), dtype=torch.bfloat16, device="cuda"))
+        torch.cuda.synchronize()
+        assert tuple(gr.dx.shape) == (0, d) and tuple(gr.dp.shape) == (0, k)
+        assert float(gr.dw1.abs().max()) == 0.0 and float(gr.dw2.abs().max()) == 0.0
