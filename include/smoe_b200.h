@@ -234,12 +234,17 @@ int smoe_ipc_close(void *dev_ptr /* the base smoe_ipc_open returned */);
  * owner q = e / experts_per_rank) is stored at row dstart[e] + i - bin_offsets[e]
  * of peer_rows[q]: x[order[i] / fan_out] (* weights[order[i]] if weights != NULL,
  * the p-weighted group of parallel_linear.py:213).  With peer_slot/peer_src the
- * row's slot id and this rank id are stored alongside (forward dispatch). */
+ * row's slot id and this rank id are stored alongside (forward dispatch), with
+ * slot_p/peer_p its routing weight slot_p[order[i]]. */
 int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_t *order,
                           const int32_t *sorted_expert, const int32_t *bin_offsets, int32_t fan_out,
                           const float *weights, int64_t n, const int64_t *dstart, int32_t experts_per_rank,
                           const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src,
-                          int32_t me, int32_t dtype, void *stream);
+                          int32_t me, const float *slot_p, const uint64_t *peer_p, int32_t dtype, void *stream);
+/* dp of received row j = sum of dp_part[j, :] (smoe_scatter2scatter_scaled
+ * partials), stored at peer_dp[recv_src[j]][recv_slot[j]] (float). */
+int smoe_ep_dp_return(const float *dp_part, int64_t n, int32_t parts, const int32_t *recv_slot,
+                      const int32_t *recv_src, const uint64_t *peer_dp, void *stream);
 /* Return: local row j goes to row recv_slot[j] of peer_out[recv_src[j]]. */
 int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv_slot, const int32_t *recv_src,
                         const uint64_t *peer_out, int32_t dtype, void *stream);

@@ -49,7 +49,8 @@ SIGNATURES = {
     "smoe_ipc_open": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p)]),
     "smoe_ipc_close": (_c.c_int, [_vp]),
     "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp,
-                                         _i32, _i32, _vp]),
+                                         _i32, _vp, _vp, _i32, _vp]),
+    "smoe_ep_dp_return": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
     "smoe_scatter2scatter_scaled": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
                                                _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),

@@ -38,7 +38,9 @@ __global__ void __launch_bounds__(kThreads) dispatch_kernel(const T *__restrict_
                                                             const int64_t *__restrict__ dstart, int e_per_rank,
                                                             const uint64_t *__restrict__ peer_rows,
                                                             const uint64_t *__restrict__ peer_slot,
-                                                            const uint64_t *__restrict__ peer_src, int me) {
+                                                            const uint64_t *__restrict__ peer_src, int me,
+                                                            const float *__restrict__ slot_p,
+                                                            const uint64_t *__restrict__ peer_p) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (i >= n) return;
@@ -63,6 +65,20 @@ __global__ void __launch_bounds__(kThreads) dispatch_kernel(const T *__restrict_
     reinterpret_cast<int32_t *>(peer_slot[q])[j] = slot;
     reinterpret_cast<int32_t *>(peer_src[q])[j] = me;
   }
+  if (lane == 0 && peer_p) reinterpret_cast<float *>(peer_p[q])[j] = slot_p[slot];
+}
+
+// dp of received row j (sum of its partials, fixed order) -> the source's
+// slot-ordered dp buffer
+__global__ void dp_return_kernel(const float *__restrict__ part, int64_t n, int parts,
+                                 const int32_t *__restrict__ recv_slot, const int32_t *__restrict__ recv_src,
+                                 const uint64_t *__restrict__ peer_dp) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const float *r = part + j * parts;
+  float s = 0.0f;
+  for (int u = 0; u < parts; ++u) s += r[u];
+  reinterpret_cast<float *>(peer_dp[recv_src[j]])[recv_slot[j]] = s;
 }
 
 // local row j -> the source rank's slot-ordered buffer, row recv_slot[j]
@@ -178,8 +194,9 @@ int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_
                           const int32_t *sorted_expert, const int32_t *bin_offsets, int32_t fan_out,
                           const float *weights, int64_t n, const int64_t *dstart, int32_t experts_per_rank,
                           const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src,
-                          int32_t me, int32_t dtype, void *stream) {
+                          int32_t me, const float *slot_p, const uint64_t *peer_p, int32_t dtype, void *stream) {
   if (fan_out < 1 || experts_per_rank < 1) return fail(SMOE_EINVAL, "ep_dispatch: fan_out and experts_per_rank >= 1");
+  if ((slot_p == nullptr) != (peer_p == nullptr)) return fail(SMOE_EINVAL, "ep_dispatch: slot_p and peer_p go together");
   if (x_rows * fan_out != n) return fail(SMOE_ESHAPE, "ep_dispatch: x rows * fan_out must equal the slot count");
   if (n == 0 || d == 0) return SMOE_OK;
   if (!x || !order || !sorted_expert || !bin_offsets || !dstart || !peer_rows)
@@ -192,11 +209,12 @@ int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_
   if (dtype == SMOE_BF16)
     dispatch_kernel<__nv_bfloat16><<<row_blocks(n), kThreads, 0, st>>>(
         (const __nv_bfloat16 *)x, d, order, sorted_expert, bin_offsets, fan_out, weights, n, dstart,
-        experts_per_rank, peer_rows, peer_slot, peer_src, me);
+        experts_per_rank, peer_rows, peer_slot, peer_src, me, slot_p, peer_p);
   else if (dtype == SMOE_F32)
     dispatch_kernel<float><<<row_blocks(n), kThreads, 0, st>>>((const float *)x, d, order, sorted_expert,
                                                                bin_offsets, fan_out, weights, n, dstart,
-                                                               experts_per_rank, peer_rows, peer_slot, peer_src, me);
+                                                               experts_per_rank, peer_rows, peer_slot, peer_src, me,
+                                                               slot_p, peer_p);
   else
     return fail(SMOE_EINVAL, "ep_dispatch: unsupported dtype");
   return check_launch("ep_dispatch_rows");
@@ -230,6 +248,15 @@ int smoe_ep_gemm_return(const void *x, int64_t n, const void *w, int32_t num_exp
   // bin offsets drive the tile schedule
   return tc_scatter2scatter_peer(x, n, w, num_experts, w_rows, w_cols, recv_slot, expert_offsets, n, transpose_w,
                                  peer_out, recv_src, recv_slot, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int smoe_ep_dp_return(const float *dp_part, int64_t n, int32_t parts, const int32_t *recv_slot,
+                      const int32_t *recv_src, const uint64_t *peer_dp, void *stream) {
+  if (n == 0) return SMOE_OK;
+  if (!dp_part || !recv_slot || !recv_src || !peer_dp || parts < 1) return fail(SMOE_EINVAL, "ep_dp_return: bad arguments");
+  dp_return_kernel<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      dp_part, n, parts, recv_slot, recv_src, peer_dp);
+  return check_launch("ep_dp_return");
 }
 
 int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,

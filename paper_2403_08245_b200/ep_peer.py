@@ -158,7 +158,7 @@ class PeerExpertParallelSmoeMlp:
     """
 
     def __init__(self, w1_local, w2_local, num_experts: int, k: int, max_tokens: int, group=None,
-                 activation: str = "gelu", timeout_s: float = 60.0):
+                 activation: str = "gelu", timeout_s: float = 60.0, scaled: bool | None = None):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -173,6 +173,11 @@ class PeerExpertParallelSmoeMlp:
         self.num_experts, self.k, self.activation = num_experts, k, activation
         self.max_tokens = max_tokens
         self.timeout_ns = int(timeout_s * 1e9)
+        # the routing weight travels with the row and moves through layer 2 at
+        # the owner (moe_layers.py's scaled form): the source's combine becomes
+        # a k-sum and dp comes back from the owner's dH epilogue
+        from . import moe_layers
+        self.scaled = moe_layers._SCALED if scaled is None else bool(scaled)
         dev = w1_local.device
         d = w1_local.shape[1]
         self.d = d
@@ -189,13 +194,13 @@ class PeerExpertParallelSmoeMlp:
         self.recv_src = SymmetricBuffer(4 * cap, dev, group)
         self.y_ret = SymmetricBuffer(esz * slots * d, dev, group)
         self.dx_ret = SymmetricBuffer(esz * slots * d, dev, group)
+        self.recv_p = SymmetricBuffer(4 * cap, dev, group)      # routing weight of each received row
+        self.dp_ret = SymmetricBuffer(4 * slots, dev, group)    # dp per slot, returned by the owners
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = [0] * _NUM_SLOTS
         # every rank must have mapped every peer buffer; decide collectively so
         # all ranks raise together (a caller can then fall back to ep.py)
-        bufs = (self.flags, self.counts, self.recv_x, self.recv_dy, self.recv_slot, self.recv_src, self.y_ret,
-                self.dx_ret)
-        errors = [b.error for b in bufs if b.error]
+        errors = [b.error for b in self._buffers() if b.error]
         gathered = [None] * g
         dist.all_gather_object(gathered, errors[0] if errors else None, group=group)
         bad = [e for e in gathered if e]
@@ -240,12 +245,14 @@ class PeerExpertParallelSmoeMlp:
         dstart, off_loc = dispatch_layout(table, self.rank)
         n_recv = int(off_loc[-1])                      # the one host sync of the step
         self._check_err()
-        # 3. dispatch rows (+ slot ids, source rank) to their owners
+        # 3. dispatch rows (+ slot ids, source rank, routing weight) to their owners
+        pw = routing.p.reshape(-1).to(torch.float32).contiguous()
         _lib.check(lib.smoe_ep_dispatch_rows(
             x.data_ptr(), t, self.d, order.o.data_ptr(), order.sorted_expert_idxs.data_ptr(),
             order.bin_offsets.data_ptr(), k, None, n, dstart.data_ptr(), e // g, self.recv_x.peers.data_ptr(),
-            self.recv_slot.peers.data_ptr(), self.recv_src.peers.data_ptr(), self.rank, _lib.SMOE_BF16,
-            _stream()), "ep_dispatch_rows")
+            self.recv_slot.peers.data_ptr(), self.recv_src.peers.data_ptr(), self.rank,
+            pw.data_ptr() if self.scaled else None, self.recv_p.peers.data_ptr() if self.scaled else None,
+            _lib.SMOE_BF16, _stream()), "ep_dispatch_rows")
         self._exchange_done(_FWD_DISPATCH)
         # 4. local experts on the landed rows (grouped in, grouped out)
         r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))[:n_recv]
@@ -254,14 +261,18 @@ class PeerExpertParallelSmoeMlp:
         de = self.w1.shape[2]
         h_pre = torch.empty((n_recv, de), dtype=x.dtype, device=x.device)
         h = torch.empty_like(h_pre)
-        K.scatter2scatter(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, out=h_pre, activation=self.activation,
-                          act_out=h)
+        if self.scaled:   # h = p * act(h_pre); order_loc is the identity, so row i's scale is recv_p[i]
+            K.scatter2scatter_scaled(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, row_scale=self._recv_p(n_recv),
+                                     activation=self.activation, out=h_pre, act_out=h)
+        else:
+            K.scatter2scatter(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, out=h_pre, activation=self.activation,
+                              act_out=h)
         # 5. layer 2, its outputs stored back into their source slots; then the
         #    routing-weighted combine at the source
         self._gemm_return(h, self.w2, order_loc, False, self.y_ret)
         self._exchange_done(_FWD_RETURN)
         y_slot = self.y_ret.view(torch.bfloat16, (self.max_tokens * k, self.d))[:n]
-        y = K.combine(routing.p, y_slot)
+        y = K.fanout_reduce(y_slot, k) if self.scaled else K.combine(routing.p, y_slot)
         ctx = PeerEpContext(order=order, p=routing.p, k=k, dstart=dstart, n_recv=n_recv, order_loc=order_loc,
                             h_pre=h_pre, h=h, y_slot=y_slot, activation=self.activation)
         return y, ctx
@@ -272,25 +283,38 @@ class PeerExpertParallelSmoeMlp:
         t = ctx.p.shape[0]
         dy = dy.contiguous()
         n = ctx.order.num_slots
-        dp = K.combine_grad_p(dy, ctx.y_slot, t, k)
+        dp = None if self.scaled else K.combine_grad_p(dy, ctx.y_slot, t, k)
         pw = ctx.p.reshape(-1).to(torch.float32).contiguous()
+        # scaled form: unweighted dY rows (p is applied in the owner's dH epilogue)
         _lib.check(lib.smoe_ep_dispatch_rows(
             dy.data_ptr(), t, self.d, ctx.order.o.data_ptr(), ctx.order.sorted_expert_idxs.data_ptr(),
-            ctx.order.bin_offsets.data_ptr(), k, pw.data_ptr(), n, ctx.dstart.data_ptr(), e // g,
-            self.recv_dy.peers.data_ptr(), None, None, self.rank, _lib.SMOE_BF16, _stream()), "ep_dispatch_rows")
+            ctx.order.bin_offsets.data_ptr(), k, None if self.scaled else pw.data_ptr(), n, ctx.dstart.data_ptr(),
+            e // g, self.recv_dy.peers.data_ptr(), None, None, self.rank, None, None, _lib.SMOE_BF16, _stream()),
+            "ep_dispatch_rows")
         self._exchange_done(_BWD_DISPATCH)
         nr = ctx.n_recv
         dyl = self.recv_dy.view(torch.bfloat16, (self.cap, self.d))[:nr]
         r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))[:nr]
         ol = ctx.order_loc
         dw2 = K.group_xty(ctx.h, dyl, ol)
-        dh = K.scatter2scatter(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=ctx.h,
-                               activation=ctx.activation, act_grad_of=ctx.h_pre)
+        if self.scaled:   # dH = p * (dY W2^T) * act'(h_pre), dp partials from the same accumulators
+            parts = torch.empty((nr, K.dp_parts(self.w1.shape[2])), dtype=torch.float32, device=dy.device)
+            dh = K.scatter2scatter_scaled(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, row_scale=self._recv_p(nr),
+                                          activation=ctx.activation, out=ctx.h, act_grad_of=ctx.h_pre,
+                                          dp_partials=parts, transpose_w=True)
+            _lib.check(lib.smoe_ep_dp_return(parts.data_ptr(), nr, parts.shape[1], self.recv_slot.local.data_ptr(),
+                                             self.recv_src.local.data_ptr(), self.dp_ret.peers.data_ptr(),
+                                             _stream()), "ep_dp_return")
+        else:
+            dh = K.scatter2scatter(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=ctx.h,
+                                   activation=ctx.activation, act_grad_of=ctx.h_pre)
         dw1 = K.group_xty(r, dh, ol)
         self._gemm_return(dh, self.w1, ol, True, self.dx_ret, scratch=dyl)
         self._exchange_done(_BWD_RETURN)
         dx_slot = self.dx_ret.view(torch.bfloat16, (self.max_tokens * k, self.d))[:n]
         dx = K.fanout_reduce(dx_slot, k)
+        if self.scaled:
+            dp = self.dp_ret.view(torch.float32, (self.max_tokens * k,))[:n].reshape(t, k).clone()
         return PeerEpGradients(dx=dx, dw1=dw1, dw2=dw2, dp=dp)
 
     def _gemm_return(self, a: torch.Tensor, w: torch.Tensor, order_loc: GroupedOrder, transpose: bool,
@@ -309,8 +333,14 @@ class PeerExpertParallelSmoeMlp:
         _lib.check(lib.smoe_ep_return_rows(out.data_ptr(), n, self.d, slot, src, dest.peers.data_ptr(),
                                            _lib.SMOE_BF16, _stream()), "ep_return_rows")
 
+    def _recv_p(self, rows: int) -> torch.Tensor:
+        return self.recv_p.view(torch.float32, (self.cap,))[:rows]
+
+    def _buffers(self):
+        return (self.flags, self.counts, self.recv_x, self.recv_dy, self.recv_slot, self.recv_src, self.y_ret,
+                self.dx_ret, self.recv_p, self.dp_ret)
+
     def close(self) -> None:
         torch.cuda.synchronize()
-        for b in (self.flags, self.counts, self.recv_x, self.recv_dy, self.recv_slot, self.recv_src, self.y_ret,
-                  self.dx_ret):
+        for b in self._buffers():
             b.close()

@@ -71,7 +71,7 @@ def _problem(world, E):
     return x, dy, w1, w2, logits
 
 
-def _worker(rank, world, port, q, fused="1", shape="c1"):
+def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
     os.environ["SMOE_EP_FUSED_RETURN"] = fused
     E, K = SHAPES[shape]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -86,14 +86,14 @@ def _worker(rank, world, port, q, fused="1", shape="c1"):
         routing = sm.topk_select(torch.softmax(logits, 1), K)
         # single-process reference on the concatenated batch
         order = sm.compute_grouped_order(routing)
-        sm.moe_layers.set_scaled(False)   # EP combines at the source, like the literal path
+        sm.moe_layers.set_scaled(scaled)   # the EP layer follows the same MLP form
         y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
         g_ref = sm.smoe_mlp_backward(c, dy)
         sl = slice(rank * T_LOCAL, (rank + 1) * T_LOCAL)
         el = E // world
         es = slice(rank * el, (rank + 1) * el)
         ep = PeerExpertParallelSmoeMlp(w1[es].contiguous(), w2[es].contiguous(), E, K, max_tokens=T_LOCAL,
-                                       timeout_s=120.0)
+                                       timeout_s=120.0, scaled=scaled)
         rt = sm.RoutingResult(routing.expert_idx[sl].contiguous(), routing.p[sl].contiguous(),
                               routing.gate_full[sl].contiguous(), renormalized=True, validate=False)
         ok = []
@@ -116,14 +116,15 @@ def _worker(rank, world, port, q, fused="1", shape="c1"):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,fused,shape", [(2, "1", "c1"), (4, "1", "c1"), (2, "0", "c1"), (4, "1", "c4"),
-                                               (2, "1", "starve")])
-def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape):
+@pytest.mark.parametrize("world,fused,shape,scaled", [
+    (2, "1", "c1", False), (4, "1", "c1", False), (2, "0", "c1", False), (4, "1", "c4", False),
+    (2, "1", "starve", False), (2, "1", "c1", True), (4, "1", "c4", True), (2, "1", "starve", True)])
+def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape, scaled):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shape)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shape, scaled)) for r in range(world)]
     for pr in procs:
         pr.start()
     results = {}
