@@ -176,6 +176,14 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # GPU leg
 
+def _max_over_ranks(v: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -260,9 +268,7 @@ def run_ours(args, rank, world, local_rank):
     launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t)
+        ms = _max_over_ranks(ms, dev)
     tokens_total = T * world
     value = tokens_total / (ms / 1e3)
     flops = flops_per_step(T, d, de, E, k)
@@ -333,9 +339,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t)
+        ms_e2e = _max_over_ranks(ms_e2e, dev)
 
     kernels = {lab: {"launches_per_step": d["launches"] / args.steps, "ms_per_launch": d["ms_per_launch"],
                      "share_of_step": d["ms_total"] / args.steps / ms}
@@ -462,6 +466,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test rig only (SMOE_BENCH_SHARE_GPU=1): every rank on GPU 0 with gloo for
+    # the host collectives, so the N>1 code path (peer-memory EP over CUDA IPC,
+    # max-over-ranks timing) runs on a one-GPU box.  Its timings are meaningless.
+    share_gpu = os.environ.get("SMOE_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local_rank = 0
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -479,7 +489,10 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
