@@ -439,6 +439,13 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches,
             "roofline": roofline,
             "roofline_gather": gather_roof,
+            # expert parallel: share of the step in exchange-only calls (dispatch
+            # stores, count exchange, completion barriers, dp return); the returns
+            # ride in the GEMM epilogues (ep_gemm_return) and are not counted here
+            "ep_exchange_share_of_step": (sum(v["share_of_step"] for lab, v in kernels.items()
+                                              if lab.startswith(("ep_dispatch", "ep_sync", "ep_put", "ep_dp_return",
+                                                                 "ep_return")))
+                                          if ep_mode == "peer" else None),
             "kernels": kernels,
             "cpu_baseline": cpu_baseline,
             "clocks": clocks,

@@ -44,6 +44,7 @@ import torch.distributed as dist
 
 from . import _lib
 from . import kernels as K
+from . import launch_timer as _lt
 from .kernels import GROUPED_TO_GROUPED
 from .router import GroupedOrder, RoutingResult, compute_grouped_order
 
@@ -58,6 +59,17 @@ _FUSED_RETURN = os.environ.get("SMOE_EP_FUSED_RETURN", "1") != "0"
 
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+def _call(label: str, fn, *args) -> None:
+    """One C-ABI call, timed under `label` when a LaunchTimer is active."""
+    t0 = _lt.begin()
+    st = fn(*args)
+    _lt.end(label, t0)
+    _lib.check(st, label)
+
+
+_SLOT_NAMES = ("ready", "counts", "fwd dispatch", "fwd return", "bwd dispatch", "bwd return")
 
 
 class SymmetricBuffer:
@@ -213,10 +225,12 @@ class PeerExpertParallelSmoeMlp:
         """Signal every peer for `slot`, then wait for every peer's signal."""
         lib = _lib.load()
         self.epoch[slot] += 1
+        t0 = _lt.begin()
         _lib.check(lib.smoe_ep_signal(self.flags.peers.data_ptr(), self.world, self.rank, slot, _stream()),
                    "ep_signal")
         _lib.check(lib.smoe_ep_wait(self.flags.local.data_ptr(), self.world, slot, self.epoch[slot],
                                     self.timeout_ns, self.err.data_ptr(), _stream()), "ep_wait")
+        _lt.end(f"ep_sync {_SLOT_NAMES[slot]}", t0)
 
     def _check_err(self) -> None:
         if int(self.err.item()):
@@ -238,8 +252,8 @@ class PeerExpertParallelSmoeMlp:
         self._exchange_done(_READY)
         # 2. count table
         cnt = order.bin_counts.to(torch.int64).contiguous()
-        _lib.check(lib.smoe_ep_put(cnt.data_ptr(), 8 * e, self.counts.peers.data_ptr(), 8 * e * self.rank, g,
-                                   _stream()), "ep_put")
+        _call("ep_put counts", lib.smoe_ep_put, cnt.data_ptr(), 8 * e, self.counts.peers.data_ptr(),
+              8 * e * self.rank, g, _stream())
         self._exchange_done(_COUNTS)
         table = self.counts.view(torch.int64, (g, e))
         dstart, off_loc = dispatch_layout(table, self.rank)
@@ -247,12 +261,12 @@ class PeerExpertParallelSmoeMlp:
         self._check_err()
         # 3. dispatch rows (+ slot ids, source rank, routing weight) to their owners
         pw = routing.p.reshape(-1).to(torch.float32).contiguous()
-        _lib.check(lib.smoe_ep_dispatch_rows(
-            x.data_ptr(), t, self.d, order.o.data_ptr(), order.sorted_expert_idxs.data_ptr(),
-            order.bin_offsets.data_ptr(), k, None, n, dstart.data_ptr(), e // g, self.recv_x.peers.data_ptr(),
-            self.recv_slot.peers.data_ptr(), self.recv_src.peers.data_ptr(), self.rank,
-            pw.data_ptr() if self.scaled else None, self.recv_p.peers.data_ptr() if self.scaled else None,
-            _lib.SMOE_BF16, _stream()), "ep_dispatch_rows")
+        _call("ep_dispatch x", lib.smoe_ep_dispatch_rows,
+              x.data_ptr(), t, self.d, order.o.data_ptr(), order.sorted_expert_idxs.data_ptr(),
+              order.bin_offsets.data_ptr(), k, None, n, dstart.data_ptr(), e // g, self.recv_x.peers.data_ptr(),
+              self.recv_slot.peers.data_ptr(), self.recv_src.peers.data_ptr(), self.rank,
+              pw.data_ptr() if self.scaled else None, self.recv_p.peers.data_ptr() if self.scaled else None,
+              _lib.SMOE_BF16, _stream())
         self._exchange_done(_FWD_DISPATCH)
         # 4. local experts on the landed rows (grouped in, grouped out)
         r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))[:n_recv]
@@ -286,11 +300,10 @@ class PeerExpertParallelSmoeMlp:
         dp = None if self.scaled else K.combine_grad_p(dy, ctx.y_slot, t, k)
         pw = ctx.p.reshape(-1).to(torch.float32).contiguous()
         # scaled form: unweighted dY rows (p is applied in the owner's dH epilogue)
-        _lib.check(lib.smoe_ep_dispatch_rows(
-            dy.data_ptr(), t, self.d, ctx.order.o.data_ptr(), ctx.order.sorted_expert_idxs.data_ptr(),
-            ctx.order.bin_offsets.data_ptr(), k, None if self.scaled else pw.data_ptr(), n, ctx.dstart.data_ptr(),
-            e // g, self.recv_dy.peers.data_ptr(), None, None, self.rank, None, None, _lib.SMOE_BF16, _stream()),
-            "ep_dispatch_rows")
+        _call("ep_dispatch dy", lib.smoe_ep_dispatch_rows,
+              dy.data_ptr(), t, self.d, ctx.order.o.data_ptr(), ctx.order.sorted_expert_idxs.data_ptr(),
+              ctx.order.bin_offsets.data_ptr(), k, None if self.scaled else pw.data_ptr(), n, ctx.dstart.data_ptr(),
+              e // g, self.recv_dy.peers.data_ptr(), None, None, self.rank, None, None, _lib.SMOE_BF16, _stream())
         self._exchange_done(_BWD_DISPATCH)
         nr = ctx.n_recv
         dyl = self.recv_dy.view(torch.bfloat16, (self.cap, self.d))[:nr]
@@ -302,9 +315,9 @@ class PeerExpertParallelSmoeMlp:
             dh = K.scatter2scatter_scaled(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, row_scale=self._recv_p(nr),
                                           activation=ctx.activation, out=ctx.h, act_grad_of=ctx.h_pre,
                                           dp_partials=parts, transpose_w=True)
-            _lib.check(lib.smoe_ep_dp_return(parts.data_ptr(), nr, parts.shape[1], self.recv_slot.local.data_ptr(),
-                                             self.recv_src.local.data_ptr(), self.dp_ret.peers.data_ptr(),
-                                             _stream()), "ep_dp_return")
+            _call("ep_dp_return", lib.smoe_ep_dp_return, parts.data_ptr(), nr, parts.shape[1],
+                  self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr(), self.dp_ret.peers.data_ptr(),
+                  _stream())
         else:
             dh = K.scatter2scatter(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=ctx.h,
                                    activation=ctx.activation, act_grad_of=ctx.h_pre)
@@ -325,13 +338,13 @@ class PeerExpertParallelSmoeMlp:
         n = a.shape[0]
         slot, src = self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr()
         if _FUSED_RETURN:
-            _lib.check(lib.smoe_ep_gemm_return(a.data_ptr(), n, w.data_ptr(), w.shape[0], w.shape[1], w.shape[2],
-                                               order_loc.bin_offsets.data_ptr(), int(transpose), slot, src,
-                                               dest.peers.data_ptr(), _stream()), "ep_gemm_return")
+            _call("ep_gemm_return " + ("W^T (dX)" if transpose else "(layer 2)"), lib.smoe_ep_gemm_return,
+                  a.data_ptr(), n, w.data_ptr(), w.shape[0], w.shape[1], w.shape[2], order_loc.bin_offsets.data_ptr(),
+                  int(transpose), slot, src, dest.peers.data_ptr(), _stream())
             return
         out = K.scatter2scatter(a, w, order_loc, 1, GROUPED_TO_GROUPED, transpose_w=transpose, out=scratch)
-        _lib.check(lib.smoe_ep_return_rows(out.data_ptr(), n, self.d, slot, src, dest.peers.data_ptr(),
-                                           _lib.SMOE_BF16, _stream()), "ep_return_rows")
+        _call("ep_return rows", lib.smoe_ep_return_rows, out.data_ptr(), n, self.d, slot, src,
+              dest.peers.data_ptr(), _lib.SMOE_BF16, _stream())
 
     def _recv_p(self, rows: int) -> torch.Tensor:
         return self.recv_p.view(torch.float32, (self.cap,))[:rows]
