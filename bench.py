@@ -78,7 +78,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -86,9 +86,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def stop(self):
+    def mark(self):
+        """Host time at the start/end of the device-timed region (after a synchronize)."""
+        return time.perf_counter()
+
+    def stop(self, window=None):
+        """Summarise the samples taken inside `window` = (t0, t1) (all samples if None):
+        idle samples before the timed region would otherwise pull the median up."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -98,7 +104,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons, watts = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for t, ln in self.lines if window is None or window[0] <= t <= window[1] + 0.05]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -253,6 +260,7 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
+    t_win0 = sampler.mark()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     from paper_2403_08245_b200.launch_timer import LaunchTimer
@@ -262,8 +270,9 @@ def run_ours(args, rank, world, local_rank):
             step(x, dy, routing)
         e1.record(st)
     torch.cuda.synchronize()
+    t_win1 = sampler.mark()
     barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop((t_win0, t_win1))
     per_kernel = lt.summary()
     launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps

@@ -45,6 +45,16 @@ constexpr int HM = TM / 2, HN = TN / 2;  // per-CTA halves
 constexpr int A_BYTES = HM * BK * 2;     // 16 KB
 constexpr int B_BYTES = HN * BK * 2;     // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+// Wide tiles (TMA-fed kernels with long K): a pair tile is 512 x 256 — each CTA
+// stages 256 A rows (two 128-row halves, one per M=256 MMA) and 128 B columns,
+// so every B stage feeds two MMAs.  Operand bytes per FLOP drop to 3/4 of the
+// 256 x 256 tile; under the B200 power cap the operand fill is ~17 % of a
+// GEMM's energy (scripts/energy.py with SMOE_TC_TIMING=5: 1.36 -> 1.64
+// TFLOP/J without fills).  The 512 accumulator columns leave no second buffer:
+// the epilogue drains the first half while the next tile's first MMAs run.
+// 48 KB stages: 4 fit beside the staging tiles.
+__host__ __device__ constexpr int wide_stages(bool staged, bool wide) { return wide ? 4 : ring_stages(staged); }
+__host__ __device__ constexpr int sig_slots(int stages) { return stages < 5 ? 5 : stages; }
 constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARPS = 8;
 constexpr int GATHER_WARPS = 4;
@@ -70,12 +80,17 @@ __host__ __device__ constexpr int kernel_threads(int am, int bm) {
   return 64 + 32 * EPI_WARPS + 32 * gather_warps(am, bm);
 }
 
-template <int AM, int BMODE, bool GK, bool STAGED>
+template <int AM, int BMODE, bool GK, bool STAGED, bool WIDE>
 __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__(2, 1, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_c2, Params p) {
   constexpr int THREADS = kernel_threads(AM, BMODE);
-  constexpr int STAGES = ring_stages(STAGED);
+  constexpr int STAGES = wide_stages(STAGED, WIDE);
+  // WIDE: 512-row pair tiles (two M=256 MMAs share each B stage; see wide_stages)
+  constexpr int TMT = WIDE ? 2 * TM : TM;           // rows per tile
+  constexpr int ABYTES = WIDE ? 2 * A_BYTES : A_BYTES;
+  constexpr int SBYTES = ABYTES + B_BYTES;          // bytes per ring stage per CTA
+  constexpr int BOXES = SBYTES / 8192;              // 64-row x 128-B boxes per stage
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-
   // critical producer and MMA warps take the highest ids and never queue behind
   // epilogue math: epilogue 0..7 | gather 8..11 (A_GATHER) | producer | MMA.
@@ -83,6 +98,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   // grouped-K with gathered operand(s): the cp.async warps fill them, TMA the rest
   constexpr bool KGATHER = GK && GATHER;
   constexpr bool GA = (AM == A_MN_G), GB = (BMODE == B_ROWS_MN_G);
+  static_assert(!WIDE || (!GATHER && STAGED), "wide tiles: TMA-fed operands, staged epilogue");
   constexpr int GW = gather_warps(AM, BMODE);
   constexpr int WP = EPI_WARPS + GW;
   constexpr int WM = WP + 1;
@@ -95,16 +111,17 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *tiles_smem = smem;
-  uint8_t *staging = smem + STAGES * STAGE_BYTES;  // [EPI_WARPS][STG_BYTES]
+  uint8_t *staging = smem + STAGES * SBYTES;  // [EPI_WARPS][STG_BYTES]
   uint64_t *bars = (uint64_t *)(staging + (STAGED ? EPI_WARPS * STG_BYTES : 0));
   uint64_t *lfull_bar = bars;                    // [STAGES]
   // relay payload (16 B) + landing slot (16 B), 16-byte aligned inside bars[STAGES, 2*STAGES)
+  constexpr int SIG = sig_slots(STAGES);        // 8-byte slots holding the relay signal
   uint8_t *signal = (uint8_t *)((((uintptr_t)(bars + STAGES)) + 15) & ~(uintptr_t)15);
-  static_assert(STAGES * 8 >= 32 + 8, "relay slots need room");
-  uint64_t *empty_bar = bars + 2 * STAGES;       // [STAGES]
-  uint64_t *tfull_bar = bars + 3 * STAGES;       // [2]
-  uint64_t *tempty_bar = bars + 3 * STAGES + 2;  // [2]
-  uint64_t *ring_full = bars + 3 * STAGES + 4;   // [RING] tile id written (both CTAs)
+  static_assert(SIG * 8 >= 32 + 8, "relay slots need room");
+  uint64_t *empty_bar = bars + STAGES + SIG;     // [STAGES]
+  uint64_t *tfull_bar = empty_bar + STAGES;      // [2]
+  uint64_t *tempty_bar = tfull_bar + 2;          // [2]
+  uint64_t *ring_full = tempty_bar + 2;          // [RING] tile id written (both CTAs)
   uint64_t *ring_empty = ring_full + RING;       // [RING] L: every consumer warp has read it
   uint32_t *s_tmem = (uint32_t *)(ring_empty + RING);
   int32_t *s_tile = (int32_t *)(ring_empty + RING + 1);      // [RING] claimed tile ids (-1 = done)
@@ -116,7 +133,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int64_t nN = (p.N + TN - 1) / TN;
-  const int64_t mM = (p.M + TM - 1) / TM;
+  const int64_t mM = (p.M + TMT - 1) / TMT;
   const int64_t cluster_id = blockIdx.x >> 1;
 
   for (int i = threadIdx.x; i <= p.E; i += THREADS) s_off[i] = p.offsets[i];
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     int64_t acc = 0;
     for (int e = 0; e < p.E; ++e) {
       s_start[e] = acc;
-      if (!GK) acc += ((s_off[e + 1] - s_off[e] + TM - 1) / TM) * nN;
+      if (!GK) acc += ((s_off[e + 1] - s_off[e] + TMT - 1) / TMT) * nN;
       else acc += mM * nN;
     }
     s_start[p.E] = acc;
@@ -209,9 +226,12 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         t = next_tile(it);
       }
       if (t < 0) break;
-      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
       const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
       const int n_half = (int)(tl.n0 + HN * rank);
+      // WIDE: rows m0+256.. (the second MMA's A operand) exist in this tile
+      const bool bot = WIDE && tl.m0 + TM < tl.m_end;
+      const int a_bytes = bot ? 2 * A_BYTES : A_BYTES;
       int gr[4] = {0, 0, 0, 0};
       const bool g4_lane = (AM == A_GATHER) && lane < TG_ROWS / 4;
       if (g4_lane) {
@@ -220,13 +240,13 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       }
       for (int kb = 0; kb < tl.nkb; ++kb) {
         const uint32_t fb = smem_u32(&lfull_bar[stage]);
-        const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+        const uint32_t sa = smem_u32(tiles_smem + stage * SBYTES);
         const int kk = kb * BK;
         // all lanes wait (keeps the warp converged, so coordinates and
         // addresses stay in uniform registers); one elected lane issues
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         if (elect_one_sync()) {
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sb = sa + ABYTES;
           if (KGATHER) {
             // this CTA's TMA bytes (non-gathered operand) are counted locally;
             // the leader also expects the peer's 16-byte relay signal
@@ -253,14 +273,22 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             // bin-tail stage of a grouped-K tile: each CTA counts its own bytes
             // locally, zeroes its rows past the bin, and the peer then signals
             // the leader (see the tail fixer below)
-            mbar_expect_tx(fb, STAGE_BYTES + (leader ? 16 : 0));
+            mbar_expect_tx(fb, B_BYTES + a_bytes + (leader ? 16 : 0));
             tma_load_2d(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
             tma_load_2d(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
             tma_load_2d(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
             tma_load_2d(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+            if (bot) {
+              tma_load_2d(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk));
+              tma_load_2d(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk));
+            }
+          } else if (p.timing == 5 && it > 0) {
+            // energy probe (SMOE_TC_TIMING=5, debug): after the first tile no
+            // operand is fetched; the MMAs run on stale shared memory
+            if (leader) mbar_arrive(fb);
           } else {
             // both CTAs' bytes are counted on the leader's barrier
-            if (leader) mbar_expect_tx(fb, 2 * STAGE_BYTES);
+            if (leader) mbar_expect_tx(fb, 2 * (B_BYTES + a_bytes));
             if (BMODE == B_W_MN) {
               tma_load_3d_cg2(&tma_b, fb, sb, n_half, kk, tl.e);
               tma_load_3d_cg2(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
@@ -272,9 +300,14 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             }
             if (AM == A_ROWS) {
               tma_load_2d_cg2(&tma_a, fb, sa, (int)(tl.k0 + kk), m_half);
+              if (bot) tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES, (int)(tl.k0 + kk), m_half + TM);
             } else if (AM == A_MN) {
               tma_load_2d_cg2(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
               tma_load_2d_cg2(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+              if (bot) {
+                tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk));
+                tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk));
+              }
             }
           }
         }
@@ -307,18 +340,23 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         if (tl.nkb == 0) continue;
         long long c0 = p.timing ? clock64() : 0;
-        mbar_wait_cluster(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+        // WIDE: one 512-column accumulator pair per tile; rows m0.. use columns
+        // [0, 256) and are drained first (tempty[0]), rows m0+256.. use [256, 512)
+        // (tempty[1]), so the next tile's first MMAs overlap the second drain
+        const int abuf = WIDE ? 0 : acc;
+        const bool bot = WIDE && tl.m0 + TM < tl.m_end;
+        mbar_wait_cluster(smem_u32(&tempty_bar[abuf]), acc_phase ^ 1);
         if (p.timing) c_tempty += clock64() - c0;
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * TN);
+        const uint32_t tmem_d = tmem_base + (uint32_t)(abuf * TN);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           long long c1 = p.timing ? clock64() : 0;
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
           if (p.timing) c_lfull += clock64() - c1;
-          uint8_t *sa_ptr = tiles_smem + stage * STAGE_BYTES;
+          uint8_t *sa_ptr = tiles_smem + stage * SBYTES;
           int nk = BK / 16;  // K16 steps issued for this stage
           if (GK && kb == tl.nkb - 1) {
             // bin tail: rows past the expert's bin belong to the next expert.
@@ -327,13 +365,13 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
-              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
+              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, BOXES, valid, 16 * nk, lane);
             }
           }
           if (RELAY) fence_proxy_async_smem();
           tc_fence_after();
           const uint32_t sa = smem_u32(sa_ptr);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sb = sa + ABYTES;
           if (elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -345,15 +383,41 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
               else bd = sdesc(sb + k * 2048, 8192, 1024);
               umma_bf16_cg2(tmem_d, ad, bd, idesc, (kb | k) != 0);
             }
+          }
+          __syncwarp();
+          if (WIDE && bot) {
+            // second MMA: rows m0+256.. (this stage's A_bot) x the same B columns
+            if (kb == 0) {
+              long long c2 = p.timing ? clock64() : 0;
+              mbar_wait_cluster(smem_u32(&tempty_bar[1]), acc_phase ^ 1);
+              if (p.timing) c_tempty += clock64() - c2;
+              tc_fence_after();
+            }
+            if (elect_one_sync()) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                if (GK && k >= nk) break;
+                uint64_t ad, bd;
+                if (AM == A_MN) ad = sdesc(sa + A_BYTES + k * 2048, 8192, 1024);
+                else ad = sdesc(sa + A_BYTES + k * 32, 16, 1024);
+                if (BMODE == B_W_K) bd = sdesc(sb + k * 32, 16, 1024);
+                else bd = sdesc(sb + k * 2048, 8192, 1024);
+                umma_bf16_cg2(tmem_d + TN, ad, bd, idesc, (kb | k) != 0);
+              }
+            }
+            __syncwarp();
+          }
+          if (elect_one_sync()) {
             umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), 0x3);
-            if (kb == tl.nkb - 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), 0x3);
+            if (kb == tl.nkb - 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[abuf]), 0x3);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (WIDE) acc_phase ^= 1;
+        else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (p.timing && lane == 0 && cluster_id < 4)
+      if (p.timing == 1 && lane == 0 && cluster_id < 4)
         printf("tc2 timing cluster %d: total %lld cyc, wait tempty %lld (%.1f%%), wait lfull %lld (%.1f%%)\n",
                (int)cluster_id, clock64() - c_start, c_tempty, 100.0 * c_tempty / (clock64() - c_start), c_lfull,
                100.0 * c_lfull / (clock64() - c_start));
@@ -368,14 +432,14 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           const int valid = (int)(tl.k_len - (int64_t)kb * BK);
           if (valid < BK) {
             mbar_wait(smem_u32(&lfull_bar[stage]), (parity_bits >> stage) & 1u);
             parity_bits ^= 1u << stage;
             const int upto = 16 * ((valid + 15) / 16);  // the leader skips K16 steps past the bin
-            if (valid < upto) zero_k_rows(tiles_smem + stage * STAGE_BYTES, 4, valid, upto, lane);
+            if (valid < upto) zero_k_rows(tiles_smem + stage * SBYTES, BOXES, valid, upto, lane);
             else fence_proxy_async_smem();
             if (elect_one_sync()) bulk_signal_cta0(smem_u32(signal + 16), smem_u32(signal), smem_u32(&lfull_bar[stage]));
             __syncwarp();
@@ -391,7 +455,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           long long w0 = p.timing ? clock64() : 0;
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
@@ -401,7 +465,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             // the next expert; zero them up to the K16 step the leader issues
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             const int upto = 16 * ((valid + 15) / 16);
-            if (valid < BK && valid < upto) zero_k_rows(tiles_smem + stage * STAGE_BYTES, 4, valid, upto, lane);
+            if (valid < BK && valid < upto) zero_k_rows(tiles_smem + stage * SBYTES, 4, valid, upto, lane);
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -436,9 +500,16 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
-        const int64_t row = tl.m0 + HM * rank + r;
-        const int64_t slab0 = tl.m0 + HM * rank + q * 32;
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
+        const bool has_acc = tl.nkb > 0;
+        // WIDE tiles drain their two 256-row halves in turn (accumulator columns
+        // [256 h, 256 h + 256)), releasing each as soon as it is read
+#pragma unroll 1
+        for (int h = 0; h < (WIDE ? 2 : 1); ++h) {
+        const int abuf = WIDE ? h : acc;
+        const int64_t mb = tl.m0 + (int64_t)TM * h;
+        const int64_t row = mb + HM * rank + r;
+        const int64_t slab0 = mb + HM * rank + q * 32;
         // a slab straddling the bin end must not touch the next expert's rows
         const bool slab_tma = tma_out && slab0 + 32 <= tl.m_end;
         const int slab_row = (int)(GK ? (int64_t)tl.e * p.M + slab0 : slab0);
@@ -462,14 +533,14 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   #pragma unroll
           for (int i = 0; i < 8; ++i) cdst[i] = cdst[i] >= 0 ? cdst[i] / p.combine_cols : -1;
         }
-        const bool has_acc = tl.nkb > 0;
-        if (has_acc) {
-          mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
+        if (has_acc && h == 0) {
+          mbar_wait_cluster(smem_u32(&tfull_bar[abuf]), acc_phase);
           tc_fence_after();
         }
-        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TN + c_begin);
+        const bool live = mb < tl.m_end;  // WIDE: the second half may lie past the bin / matrix
   #pragma unroll 1
-        for (int cg = 0; cg < EPI_COLS; cg += 64) {
+        for (int cg = 0; live && cg < EPI_COLS; cg += 64) {
           const int64_t col0 = tl.n0 + c_begin + cg;
           const bool col_ok = col0 + cc * 8 < p.N;
           if (col0 >= p.N) break;
@@ -570,10 +641,14 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (leader) mbar_arrive(smem_u32(&tempty_bar[acc]));
-            else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+            if (leader) mbar_arrive(smem_u32(&tempty_bar[abuf]));
+            else mbar_arrive_cluster(smem_u32(&tempty_bar[abuf]), 0);
           }
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        }  // halves
+        if (has_acc) {
+          if (WIDE) acc_phase ^= 1;
+          else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
       if (lane == 0) bulk_wait0();
@@ -588,7 +663,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int it = 0;; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
-        const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         const int64_t row = tl.m0 + HM * rank + r;
         const bool valid = row < tl.m_end;
         __nv_bfloat16 *orow = nullptr, *orow2 = nullptr;
@@ -667,7 +742,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     for (int it = 0;; ++it) {
       const int64_t t = next_tile(it);
       if (t < 0) break;
-      const Tile tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
       const int64_t acol = tl.m0 + HM * rank + chunk * 8;
       const int64_t bcol = tl.n0 + HN * rank + chunk * 8;
       const bool a_ok = acol < p.M, b_ok = bcol < p.N;
@@ -710,8 +785,8 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           const uint32_t mine = pf[j] >= 0 ? ((uint32_t)pf[j] / fdiv) * rchunks : 0x80000000u;
           pf[j] = ld_slot(kb + IDX_PF);
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-          const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa = smem_u32(tiles_smem + stage * SBYTES);
+          const uint32_t sb = sa + ABYTES;
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
             if (GA) {
@@ -746,7 +821,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     Tile tl{};
     int32_t cur[G_RPT] = {}, nxt[G_RPT] = {};
     if (t >= 0) {
-      tl = decode_tile<GK, TM, TN>(t, p, s_start, s_off, nN, mM);
+      tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
       load_rows(tl, cur);
     }
     for (int it = 0; t >= 0; ++it) {
@@ -755,7 +830,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       auto prefetch_next = [&]() {
         t_n = next_tile(it + 1);
         if (t_n >= 0) {
-          tl_n = decode_tile<GK, TM, TN>(t_n, p, s_start, s_off, nN, mM);
+          tl_n = decode_tile<GK, TMT, TN>(t_n, p, s_start, s_off, nN, mM);
           load_rows(tl_n, nxt);
         }
       };
@@ -764,7 +839,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int j = 0; j < G_RPT; ++j) src[j] = p.x + (int64_t)(cur[j] / p.fan_out) * p.K + chunk * 8;
       for (int kb = 0; kb < tl.nkb; ++kb) {
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-        const uint32_t sa = smem_u32(tiles_smem + stage * STAGE_BYTES);
+        const uint32_t sa = smem_u32(tiles_smem + stage * SBYTES);
         const int64_t col = (int64_t)kb * BK;
         const bool ok = col + chunk * 8 < p.K;
 #pragma unroll
@@ -807,16 +882,17 @@ static int group_m_k_setting() {
   return gm;
 }
 
-static size_t smem_bytes(int E, bool staged) {
-  const int stages = ring_stages(staged);
-  return 1024 + stages * STAGE_BYTES + (staged ? EPI_WARPS * STG_BYTES : 0) + 8 * (3 * stages + 4 + 2 * RING + 2 + RING / 2) +
+static size_t smem_bytes(int E, bool staged, bool wide = false) {
+  const int stages = wide_stages(staged, wide);
+  return 1024 + stages * (wide ? STAGE_BYTES + A_BYTES : STAGE_BYTES) + (staged ? EPI_WARPS * STG_BYTES : 0) + 8 * (2 * stages + sig_slots(stages) + 4 + 2 * RING + 2 + RING / 2) +
          12 * (E + 1) + 64;
 }
 
 }  // namespace tc2
 
 bool tc2_supports_experts(int E) {
-  return tc2::smem_bytes(E, true) <= 232448 && tc2::smem_bytes(E, false) <= 232448;
+  return tc2::smem_bytes(E, true) <= 232448 && tc2::smem_bytes(E, false) <= 232448 &&
+         tc2::smem_bytes(E, true, true) <= 232448;
 }
 
 namespace tc2 {
@@ -835,11 +911,11 @@ static uint32_t *tile_counter(cudaStream_t st) {
   return c;
 }
 
-template <int AM, int BMODE, bool GK, bool STAGED>
+template <int AM, int BMODE, bool GK, bool STAGED, bool WIDE = false>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &tc, const CUtensorMap &tc2,
                   const Params &p, int64_t max_tiles, cudaStream_t st) {
-  auto kern = tc2_gemm_kernel<AM, BMODE, GK, STAGED>;
-  size_t smem = smem_bytes(p.E, STAGED);
+  auto kern = tc2_gemm_kernel<AM, BMODE, GK, STAGED, WIDE>;
+  size_t smem = smem_bytes(p.E, STAGED, WIDE);
   static size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -873,6 +949,32 @@ static bool staged_for(bool gather, bool grouped_out, int64_t K) {
     small_k = k ? atoll(k) : 1024;
   }
   return gather || (all && grouped_out) || K <= small_k;
+}
+
+// Wide 512-row tiles (see wide_stages) for the TMA-fed kernels whose K is long
+// enough to hide the exposed part of the epilogue: the next tile's MMAs wait
+// for the first half's drain, its second MMA for the second half's.  C1
+// (SMOE_TC_TIMING=1, MMA-issuer wait on the epilogue): K = 14336 4.3 %, the
+// grouped-K dW GEMMs (bins of 8192) 5.0 %, K = 4096 10.8 %, and 42 % for the
+// act-grad epilogue (it reads h_pre) at K = 4096 — so wide tiles go to plain
+// epilogues with K >= 8192 (scripts/wide_ab.sh, profiles/r1_wide_tiles.txt).
+// SMOE_TC_WIDE=0 disables them, =1 forces them whenever the kernel allows.
+static int wide_mode() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char *env = getenv("SMOE_TC_WIDE");
+    mode = env ? atoi(env) : -1;
+  }
+  return mode;
+}
+static bool wide_for(int64_t K, int epi, bool grouped_k = false) {
+  if (wide_mode() >= 0) return wide_mode() == 1;
+  static int64_t min_k = -1;  // SMOE_TC_WIDE_MIN_K: K threshold of the grouped-M kernels
+  if (min_k < 0) {
+    const char *env = getenv("SMOE_TC_WIDE_MIN_K");
+    min_k = env ? atoll(env) : 8192;
+  }
+  return K >= (grouped_k ? 8192 : min_k) && epi != SMOE_EPI_ACT_GRAD && epi != SMOE_EPI_ACT_GRAD_SCALED;
 }
 
 // Row-blocks (256 rows) per raster band of the grouped-M schedule.  With the
@@ -950,6 +1052,12 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
+    if (epi != EPI_COMBINE && !peer_out && wide_for(d_in, epi)) {
+      const int64_t wide_tiles = ((n + 2 * TM - 1) / (2 * TM) + E) * ((d_out + TN - 1) / TN);
+      p.group_m = (p.group_m + 1) / 2;  // bands in 512-row blocks
+      if (!trans) return launch<A_ROWS, B_W_MN, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
+      return launch<A_ROWS, B_W_K, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
+    }
     if (epi == EPI_COMBINE || peer_out || staged_for(false, gout, d_in)) {
       if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
       return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
@@ -1029,6 +1137,11 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
   CUtensorMap tc;
   if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
+  if (wide_for(E > 0 ? n / E : 0, SMOE_EPI_NONE, true)) {  // K = the bins, 8192 rows on average at C1
+    const int64_t wide_tiles = (int64_t)E * ((d_in + 2 * TM - 1) / (2 * TM)) * ((d_out + TN - 1) / TN);
+    p.group_m = (p.group_m + 1) / 2;
+    return launch<A_MN, B_ROWS_MN, true, true, true>(ta, tb, tc, tc, p, wide_tiles, st);
+  }
   if (staged_for(false, true, INT64_MAX)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);
   return launch<A_MN, B_ROWS_MN, true, false>(ta, tb, tc, tc, p, max_tiles, st);
 }
