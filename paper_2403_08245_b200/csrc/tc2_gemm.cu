@@ -337,21 +337,109 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       uint32_t acc_phase = 0;
       // p.timing: per-cluster cycle counters of the issue loop (SMOE_TC_TIMING=1, debug)
       long long c_start = clock64(), c_tempty = 0, c_lfull = 0;
-      for (int it = 0;; ++it) {
+      // WIDE issue order.  A tile's stages are issued in groups: MMA#1 (rows
+      // m0.., accumulator columns [0, 256)) for every stage of the group, then
+      // MMA#2 (rows m0+256.., columns [256, 512)) for the same stages, each
+      // stage released after its MMA#2.  The first group (up to `defer`
+      // stages) lets MMA#1 run while the epilogue still drains the previous
+      // tile's second half; the last group completes the first half `defer`
+      // stages early (tfull[0] before tfull[1]), so its drain overlaps the
+      // tile's final MMA#2s.  Middle groups are single stages.
+      auto wide_group = [&](const Tile &tl, bool bot, int kb0, int kb1, bool first, bool last, int &stage,
+                            uint32_t &phase, long long &c_lfull, long long &c_tempty) {
+        const int st0 = stage;
+        int nk_last = BK / 16;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          long long c1 = p.timing ? clock64() : 0;
+          mbar_wait(smem_u32(&lfull_bar[stage]), phase);
+          if (p.timing) c_lfull += clock64() - c1;
+          uint8_t *sa_ptr = tiles_smem + stage * SBYTES;
+          int nk = BK / 16;
+          if (GK && kb == tl.nkb - 1) {
+            const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+            if (valid < BK) {
+              nk = (valid + 15) / 16;
+              if (valid < 16 * nk) zero_k_rows(sa_ptr, BOXES, valid, 16 * nk, lane);
+            }
+            nk_last = nk;
+          }
+          tc_fence_after();
+          const uint32_t sa = smem_u32(sa_ptr), sb = sa + ABYTES;
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              if (GK && k >= nk) break;
+              const uint64_t ad = AM == A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
+              const uint64_t bd = BMODE == B_W_K ? sdesc(sb + k * 32, 16, 1024) : sdesc(sb + k * 2048, 8192, 1024);
+              umma_bf16_cg2(tmem_base, ad, bd, idesc, (kb | k) != 0);
+            }
+            if (!bot) umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (last && elect_one_sync()) {
+          umma_commit_cg2_mc(smem_u32(&tfull_bar[0]), 0x3);
+          if (!bot) umma_commit_cg2_mc(smem_u32(&tfull_bar[1]), 0x3);
+        }
+        __syncwarp();
+        if (!bot) return;
+        if (first) {
+          long long c2 = p.timing ? clock64() : 0;
+          mbar_wait_cluster(smem_u32(&tempty_bar[1]), acc_phase ^ 1);
+          if (p.timing) c_tempty += clock64() - c2;
+          tc_fence_after();
+        }
+        int sg = st0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int nk = (GK && kb == tl.nkb - 1) ? nk_last : BK / 16;
+          const uint32_t sa = smem_u32(tiles_smem + sg * SBYTES), sb = sa + ABYTES;
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              if (GK && k >= nk) break;
+              const uint64_t ad = AM == A_MN ? sdesc(sa + A_BYTES + k * 2048, 8192, 1024)
+                                             : sdesc(sa + A_BYTES + k * 32, 16, 1024);
+              const uint64_t bd = BMODE == B_W_K ? sdesc(sb + k * 32, 16, 1024) : sdesc(sb + k * 2048, 8192, 1024);
+              umma_bf16_cg2(tmem_base + TN, ad, bd, idesc, (kb | k) != 0);
+            }
+            umma_commit_cg2_mc(smem_u32(&empty_bar[sg]), 0x3);
+          }
+          __syncwarp();
+          if (++sg == STAGES) sg = 0;
+        }
+        if (last && elect_one_sync()) umma_commit_cg2_mc(smem_u32(&tfull_bar[1]), 0x3);
+        __syncwarp();
+      };
+      const int defer = p.wide_defer < 1 ? 1 : (p.wide_defer > STAGES ? STAGES : p.wide_defer);
+      for (int it = 0; WIDE; ++it) {
+        const int64_t t = next_tile(it);
+        if (t < 0) break;
+        const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
+        if (tl.nkb == 0) continue;
+        const bool bot = tl.m0 + TM < tl.m_end;
+        long long c0 = p.timing ? clock64() : 0;
+        mbar_wait_cluster(smem_u32(&tempty_bar[0]), acc_phase ^ 1);
+        if (p.timing) c_tempty += clock64() - c0;
+        tc_fence_after();
+        const int n = tl.nkb;
+        const int h1 = n < defer ? n : defer;            // first group [0, h1)
+        const int t0 = n - defer > h1 ? n - defer : h1;  // last group [t0, n) (empty if t0 == n)
+        wide_group(tl, bot, 0, h1, true, h1 == n, stage, phase, c_lfull, c_tempty);
+        for (int kb = h1; kb < t0; ++kb) wide_group(tl, bot, kb, kb + 1, false, false, stage, phase, c_lfull, c_tempty);
+        if (t0 < n) wide_group(tl, bot, t0, n, false, true, stage, phase, c_lfull, c_tempty);
+        acc_phase ^= 1;
+      }
+      for (int it = 0; !WIDE; ++it) {
         const int64_t t = next_tile(it);
         if (t < 0) break;
         const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         if (tl.nkb == 0) continue;
         long long c0 = p.timing ? clock64() : 0;
-        // WIDE: one 512-column accumulator pair per tile; rows m0.. use columns
-        // [0, 256) and are drained first (tempty[0]), rows m0+256.. use [256, 512)
-        // (tempty[1]), so the next tile's first MMAs overlap the second drain
-        const int abuf = WIDE ? 0 : acc;
-        const bool bot = WIDE && tl.m0 + TM < tl.m_end;
-        mbar_wait_cluster(smem_u32(&tempty_bar[abuf]), acc_phase ^ 1);
+        mbar_wait_cluster(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
         if (p.timing) c_tempty += clock64() - c0;
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(abuf * TN);
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * TN);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           long long c1 = p.timing ? clock64() : 0;
           mbar_wait(smem_u32(&lfull_bar[stage]), phase);
@@ -365,7 +453,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
-              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, BOXES, valid, 16 * nk, lane);
+              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
             }
           }
           if (RELAY) fence_proxy_async_smem();
@@ -383,39 +471,13 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
               else bd = sdesc(sb + k * 2048, 8192, 1024);
               umma_bf16_cg2(tmem_d, ad, bd, idesc, (kb | k) != 0);
             }
-          }
-          __syncwarp();
-          if (WIDE && bot) {
-            // second MMA: rows m0+256.. (this stage's A_bot) x the same B columns
-            if (kb == 0) {
-              long long c2 = p.timing ? clock64() : 0;
-              mbar_wait_cluster(smem_u32(&tempty_bar[1]), acc_phase ^ 1);
-              if (p.timing) c_tempty += clock64() - c2;
-              tc_fence_after();
-            }
-            if (elect_one_sync()) {
-#pragma unroll
-              for (int k = 0; k < BK / 16; ++k) {
-                if (GK && k >= nk) break;
-                uint64_t ad, bd;
-                if (AM == A_MN) ad = sdesc(sa + A_BYTES + k * 2048, 8192, 1024);
-                else ad = sdesc(sa + A_BYTES + k * 32, 16, 1024);
-                if (BMODE == B_W_K) bd = sdesc(sb + k * 32, 16, 1024);
-                else bd = sdesc(sb + k * 2048, 8192, 1024);
-                umma_bf16_cg2(tmem_d + TN, ad, bd, idesc, (kb | k) != 0);
-              }
-            }
-            __syncwarp();
-          }
-          if (elect_one_sync()) {
             umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), 0x3);
-            if (kb == tl.nkb - 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[abuf]), 0x3);
+            if (kb == tl.nkb - 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), 0x3);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (WIDE) acc_phase ^= 1;
-        else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if (p.timing == 1 && lane == 0 && cluster_id < 4)
         printf("tc2 timing cluster %d: total %lld cyc, wait tempty %lld (%.1f%%), wait lfull %lld (%.1f%%)\n",
@@ -533,7 +595,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   #pragma unroll
           for (int i = 0; i < 8; ++i) cdst[i] = cdst[i] >= 0 ? cdst[i] / p.combine_cols : -1;
         }
-        if (has_acc && h == 0) {
+        if (has_acc && (WIDE || h == 0)) {  // WIDE: each half has its own tfull
           mbar_wait_cluster(smem_u32(&tfull_bar[abuf]), acc_phase);
           tc_fence_after();
         }
@@ -967,6 +1029,15 @@ static int wide_mode() {
   }
   return mode;
 }
+// Stages per first / last MMA group of a wide tile (SMOE_TC_WIDE_DEFER, 1..4).
+static int wide_defer() {
+  static int d = -1;
+  if (d < 0) {
+    const char *env = getenv("SMOE_TC_WIDE_DEFER");
+    d = env ? atoi(env) : 4;
+  }
+  return d;
+}
 static bool wide_for(int64_t K, int epi, bool grouped_k = false) {
   if (wide_mode() >= 0) return wide_mode() == 1;
   static int64_t min_k = -1;  // SMOE_TC_WIDE_MIN_K: K threshold of the grouped-M kernels
@@ -1055,6 +1126,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (epi != EPI_COMBINE && !peer_out && wide_for(d_in, epi)) {
       const int64_t wide_tiles = ((n + 2 * TM - 1) / (2 * TM) + E) * ((d_out + TN - 1) / TN);
       p.group_m = (p.group_m + 1) / 2;  // bands in 512-row blocks
+      p.wide_defer = wide_defer();
       if (!trans) return launch<A_ROWS, B_W_MN, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
       return launch<A_ROWS, B_W_K, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
     }
@@ -1140,6 +1212,7 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   if (wide_for(E > 0 ? n / E : 0, SMOE_EPI_NONE, true)) {  // K = the bins, 8192 rows on average at C1
     const int64_t wide_tiles = (int64_t)E * ((d_in + 2 * TM - 1) / (2 * TM)) * ((d_out + TN - 1) / TN);
     p.group_m = (p.group_m + 1) / 2;
+    p.wide_defer = wide_defer();
     return launch<A_MN, B_ROWS_MN, true, true, true>(ta, tb, tc, tc, p, wide_tiles, st);
   }
   if (staged_for(false, true, INT64_MAX)) return launch<A_MN, B_ROWS_MN, true, true>(ta, tb, tc, tc, p, max_tiles, st);

@@ -48,6 +48,7 @@ struct Params {
   const int32_t *row_slot;
   float *dp_part;          // EPI_ACT_GRAD_SCALED: [M, dp_parts] partial dot products
   int dp_parts;
+  int wide_defer;          // tc2 wide tiles: stages per first / last MMA group
 };
 
 __device__ __forceinline__ bool epi_scaled(int epi) {
