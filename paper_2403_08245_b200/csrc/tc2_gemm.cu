@@ -1019,7 +1019,8 @@ static bool staged_for(bool gather, bool grouped_out, int64_t K) {
 // (SMOE_TC_TIMING=1, MMA-issuer wait on the epilogue): K = 14336 4.3 %, the
 // grouped-K dW GEMMs (bins of 8192) 5.0 %, K = 4096 10.8 %, and 42 % for the
 // act-grad epilogue (it reads h_pre) at K = 4096 — so wide tiles go to plain
-// epilogues with K >= 8192 (scripts/wide_ab.sh, profiles/r1_wide_tiles.txt).
+// epilogues with K >= 8192 and to the dW GEMMs with bins >= 4096 rows (C2: +0.8 %;
+// scripts/wide_ab*.sh, scripts/wide_c2.sh, profiles/r1_wide_tiles.txt).
 // SMOE_TC_WIDE=0 disables them, =1 forces them whenever the kernel allows.
 static int wide_mode() {
   static int mode = -2;
@@ -1040,12 +1041,16 @@ static int wide_defer() {
 }
 static bool wide_for(int64_t K, int epi, bool grouped_k = false) {
   if (wide_mode() >= 0) return wide_mode() == 1;
-  static int64_t min_k = -1;  // SMOE_TC_WIDE_MIN_K: K threshold of the grouped-M kernels
+  // K thresholds: SMOE_TC_WIDE_MIN_K (grouped-M kernels), SMOE_TC_WIDE_MIN_BIN
+  // (grouped-K kernels, mean bin length)
+  static int64_t min_k = -1, min_bin = -1;
   if (min_k < 0) {
     const char *env = getenv("SMOE_TC_WIDE_MIN_K");
     min_k = env ? atoll(env) : 8192;
+    env = getenv("SMOE_TC_WIDE_MIN_BIN");
+    min_bin = env ? atoll(env) : 4096;
   }
-  return K >= (grouped_k ? 8192 : min_k) && epi != SMOE_EPI_ACT_GRAD && epi != SMOE_EPI_ACT_GRAD_SCALED;
+  return K >= (grouped_k ? min_bin : min_k) && epi != SMOE_EPI_ACT_GRAD && epi != SMOE_EPI_ACT_GRAD_SCALED;
 }
 
 // Row-blocks (256 rows) per raster band of the grouped-M schedule.  With the
