@@ -17,9 +17,14 @@ def main(path, only_ours=True):
         if only_ours and "smoe" not in name and "gemm_kernel" not in name:
             continue
         short = re.sub(r"\(.*", "", name)
-        m = re.search(r"(tc2?)_gemm_kernel<(\d+), (\d+), (\w+)>", name)
+        m = re.search(r"(tc2?)_gemm_kernel<(\d+), (\d+), (\w+)(?:, (\w+))?(?:, (\w+))?>", name)
         if m:
-            short = f"{m.group(1)}_gemm<A{m.group(2)},B{m.group(3)},GK={m.group(4)}>"
+            short = f"{m.group(1)}_gemm<A{m.group(2)},B{m.group(3)},GK={m.group(4)}"
+            if m.group(5) is not None:
+                short += f",STAGED={m.group(5)}"
+            if m.group(6) is not None:
+                short += f",WIDE={m.group(6)}"
+            short += ">"
         out.append((int(r[ii]), short, float(r[vi].replace(",", "")) / 1e3))
     for i, s, us in out:
         print(f"{i:5d} {us:10.1f} us  {s}")
