@@ -128,3 +128,53 @@ torch.save((h.cpu(), a.cpu(), g.cpu(), dw.cpu()), sys.argv[1])
         outs.append(torch.load(path))
     for u, v in zip(*outs):
         assert torch.equal(u, v)
+
+
+def test_wide_tiles_match_256_row_tiles(tmp_path):
+    """Wide 512 x 256 pair tiles (SMOE_TC_WIDE=1: two M=256 MMAs per B stage,
+    grouped MMA issue) are bit-identical to the 256 x 256 tiles (SMOE_TC_WIDE=0):
+    the same K16 products accumulate in the same order per output element.
+    Covers bins shorter than half a wide tile (second MMA skipped), bins that
+    are not multiples of 512, empty experts, K tails of the grouped-K kernel,
+    N tails, the scaled / activation / act-grad epilogues, scattered outputs,
+    and both group-issue depths (SMOE_TC_WIDE_DEFER=1 and 4)."""
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2403_08245_b200 as sm
+torch.manual_seed(2)
+outs = []
+for (t, k, e, d, de) in ((2100, 2, 8, 264, 584), (700, 3, 16, 136, 1032), (37, 1, 4, 64, 256)):
+    ids = torch.stack([torch.randperm(e - 1)[:k] for _ in range(t)]).cuda()   # expert e-1 stays empty
+    p = torch.rand(t, k, device='cuda') + 0.1
+    r = sm.RoutingResult(ids, p, torch.zeros(t, e, device='cuda'), renormalized=False, validate=False)
+    o = sm.compute_grouped_order(r)
+    n = t * k
+    xg = (torch.rand(n, d, device='cuda') * 2 - 1).bfloat16()
+    w = ((torch.rand(e, d, de, device='cuda') * 2 - 1) / 16).bfloat16()
+    wt = ((torch.rand(e, de, d, device='cuda') * 2 - 1) / 16).bfloat16()
+    h = torch.empty(n, de, device='cuda', dtype=torch.bfloat16)
+    a = torch.empty_like(h)
+    sm.scatter2scatter(xg, w, o, 1, sm.GROUPED_TO_GROUPED, out=h, activation='gelu', act_out=a, engine='tcgen05')
+    outs += [h, a]
+    outs.append(sm.scatter2scatter(xg, w, o, 1, sm.GROUPED_TO_SCATTERED, engine='tcgen05'))
+    outs.append(sm.scatter2scatter(h, wt, o, 1, sm.GROUPED_TO_SCATTERED, engine='tcgen05'))
+    outs.append(sm.scatter2scatter(xg, wt, o, 1, sm.GROUPED_TO_GROUPED, transpose_w=True, engine='tcgen05'))
+    outs.append(sm.scatter2scatter(xg, w, o, 1, sm.GROUPED_TO_GROUPED, activation='gelu', act_grad_of=h,
+                                   engine='tcgen05'))
+    pf = p.reshape(-1).float().contiguous()
+    outs.append(sm.kernels.scatter2scatter_scaled(xg, w, o, 1, sm.GROUPED_TO_GROUPED, row_scale=pf,
+                                                  activation='gelu', out=torch.empty_like(h), act_out=a.clone()))
+    outs.append(sm.group_xty(xg, h, o, engine='tcgen05'))
+    outs.append(sm.group_xty(h, xg, o, engine='tcgen05'))
+torch.save([x.cpu() for x in outs], sys.argv[1])
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for tag, env_add in (("off", {"SMOE_TC_WIDE": "0"}), ("wide4", {"SMOE_TC_WIDE": "1"}),
+                         ("wide1", {"SMOE_TC_WIDE": "1", "SMOE_TC_WIDE_DEFER": "1"})):
+        path = str(tmp_path / f"wide_{tag}.pt")
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env_add), timeout=300)
+        runs[tag] = torch.load(path)
+    for tag in ("wide4", "wide1"):
+        for i, (u, v) in enumerate(zip(runs["off"], runs[tag])):
+            assert torch.equal(u, v), (tag, i)
