@@ -250,17 +250,21 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    # clocks are sampled from the start of the warm-up (the GPU is under the same
+    # load there) to the end of the timed steps, so short timed regions still
+    # get several nvidia-smi samples; idle time before the warm-up is excluded
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.2)    # nvidia-smi start-up
+    torch.cuda.synchronize()
+    t_win0 = sampler.mark()
     for _ in range(args.warmup):
         step(x, dy, routing)
     torch.cuda.synchronize()
     barrier()
     launches0 = _lib.launch_count()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
-    t_win0 = sampler.mark()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     from paper_2403_08245_b200.launch_timer import LaunchTimer
@@ -273,6 +277,7 @@ def run_ours(args, rank, world, local_rank):
     t_win1 = sampler.mark()
     barrier()
     clocks = sampler.stop((t_win0, t_win1))
+    clocks["window"] = "warm-up + timed steps"
     per_kernel = lt.summary()
     launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
