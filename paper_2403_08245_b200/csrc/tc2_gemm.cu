@@ -600,7 +600,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           tc_fence_after();
         }
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TN + c_begin);
-        const bool live = mb < tl.m_end;  // WIDE: the second half may lie past the bin / matrix
+        // WIDE: the second half may lie past the bin / matrix.  SMOE_TC_TIMING=6
+        // (debug probe): no epilogue work at all, accumulators released unread.
+        const bool live = mb < tl.m_end && p.timing != 6;
   #pragma unroll 1
         for (int cg = 0; live && cg < EPI_COLS; cg += 64) {
           const int64_t col0 = tl.n0 + c_begin + cg;
@@ -755,7 +757,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         }
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
   #pragma unroll 1
-        for (int c = 0; c < EPI_COLS; c += 16) {
+        for (int c = 0; c < (p.timing == 6 ? 0 : EPI_COLS); c += 16) {
           uint32_t v[16];
           if (has_acc) {
             tmem_ld16(tbase + c, v);
@@ -1001,16 +1003,23 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
 // Short-K GEMMs (K <= SMOE_TC_STAGE_K, default 1024: the MoMHA projections'
 // d_proj = 512 side) are epilogue-bound, so they stage too: a tile's mainloop
 // is only K/64 ring stages long and the 7th stage buys nothing.
+// Scattered-output kernels stage too (SMOE_TC_STAGE_SCATTERED=0 turns it off):
+// row-per-thread stores to scattered slots cost the C2 K = 1792 layer-2 / dX
+// GEMMs 6 % of tensor-pipe activity (86 % vs 92 % with the epilogue removed,
+// SMOE_TC_TIMING=6); staged, coalesced row segments take them to 88 % and
+// 2.75 -> 2.66 ms (scripts/c2_epi_variants.sh).
 static bool staged_for(bool gather, bool grouped_out, int64_t K) {
-  static int all = -1;
+  static int all = -1, scattered = -1;
   static int64_t small_k = -1;
   if (all < 0) {
     const char *env = getenv("SMOE_TC_EPI");
     all = (env && !strcmp(env, "all")) ? 1 : 0;
     const char *k = getenv("SMOE_TC_STAGE_K");
     small_k = k ? atoll(k) : 1024;
+    const char *sc = getenv("SMOE_TC_STAGE_SCATTERED");
+    scattered = sc ? atoi(sc) : 1;
   }
-  return gather || (all && grouped_out) || K <= small_k;
+  return gather || (all && grouped_out) || K <= small_k || (scattered && !grouped_out);
 }
 
 // Wide 512-row tiles (see wide_stages) for the TMA-fed kernels whose K is long

@@ -8,7 +8,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2403_08245_b200 as sm  # noqa: E402
 
 which = sys.argv[1]
-T, d, de, E, k = 32768, 4096, 14336, 8, 2
+import os  # noqa: E402
+# SMOE_PROF_CFG=C2: the fine-grained config (E=64, k=8, d_expert=1792); default C1
+T, d, de, E, k = (32768, 4096, 1792, 64, 8) if os.environ.get("SMOE_PROF_CFG") == "C2" else (32768, 4096, 14336, 8, 2)
 n = T * k
 dev = "cuda"
 g = torch.Generator(device=dev).manual_seed(0)
