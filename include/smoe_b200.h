@@ -46,7 +46,10 @@ typedef enum {
 typedef enum { SMOE_F32 = 0, SMOE_BF16 = 1 } smoe_dtype;
 
 /* Activations of moe_layers.py:42-72 (exact-erf GELU, ReLU, SiLU). */
-typedef enum { SMOE_ACT_GELU = 0, SMOE_ACT_RELU = 1, SMOE_ACT_SILU = 2 } smoe_activation;
+typedef enum { SMOE_ACT_GELU = 0, SMOE_ACT_RELU = 1, SMOE_ACT_SILU = 2,
+               /* identity: only for smoe_scatter2scatter_scaled (a routed linear with
+                  combine weights; the dp partials of its input-gradient epilogue) */
+               SMOE_ACT_IDENTITY = 3 } smoe_activation;
 
 /* scatter2scatter epilogues (fusions of moe_layers.py:169-175 and :205-206). */
 typedef enum {

@@ -21,6 +21,7 @@ LIB_PATH = Path(os.environ["SMOE_LIB"]) if os.environ.get("SMOE_LIB") else _PKG 
 SMOE_OK, SMOE_EINVAL, SMOE_ESHAPE, SMOE_ECUDA, SMOE_ENOTSUP = range(5)
 SMOE_F32, SMOE_BF16 = 0, 1
 ACTIVATION_IDS = {"gelu": 0, "relu": 1, "silu": 2}
+ACT_IDENTITY = 3   # scatter2scatter_scaled only (routed linear with combine weights)
 EPI_NONE, EPI_ACT, EPI_ACT_GRAD, EPI_ACT_ONLY, EPI_ACT_SCALED, EPI_ACT_GRAD_SCALED = 0, 1, 2, 3, 4, 5
 ENGINE_IDS = {"auto": 0, "simt": 1, "tcgen05": 2}
 

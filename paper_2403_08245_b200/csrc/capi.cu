@@ -237,7 +237,7 @@ int smoe_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, in
                                 void *out2, const void *aux, float *dp_part, int32_t dp_parts, void *stream) {
   REQUIRE(epilogue == SMOE_EPI_ACT_SCALED || epilogue == SMOE_EPI_ACT_GRAD_SCALED, SMOE_EINVAL,
           "scatter2scatter_scaled takes SMOE_EPI_ACT_SCALED or SMOE_EPI_ACT_GRAD_SCALED");
-  REQUIRE(activation >= SMOE_ACT_GELU && activation <= SMOE_ACT_SILU, SMOE_EINVAL, "bad activation");
+  REQUIRE(activation >= SMOE_ACT_GELU && activation <= SMOE_ACT_IDENTITY, SMOE_EINVAL, "bad activation");
   REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
   if (grouped_in)
     REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");

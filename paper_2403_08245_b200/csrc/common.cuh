@@ -32,6 +32,7 @@ template <> struct Num<__nv_bfloat16> {
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == SMOE_ACT_GELU) return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));
   if (act == SMOE_ACT_RELU) return z > 0.0f ? z : 0.0f;
+  if (act == SMOE_ACT_IDENTITY) return z;
   // SiLU
   return z / (1.0f + expf(-z));
 }
@@ -41,6 +42,7 @@ __device__ __forceinline__ float act_grad(int act, float z) {
     return 0.5f * (1.0f + erff(z * 0.70710678118654752f)) +
            z * expf(-0.5f * z * z) * 0.39894228040143268f;
   if (act == SMOE_ACT_RELU) return z > 0.0f ? 1.0f : 0.0f;
+  if (act == SMOE_ACT_IDENTITY) return 1.0f;
   float s = 1.0f / (1.0f + expf(-z));
   return s * (1.0f + z * (1.0f - s));
 }
@@ -73,6 +75,7 @@ __device__ __forceinline__ float act_fwd_fast(int act, float z) {
     return 0.5f * z * (1.0f + r.erf);
   }
   if (act == SMOE_ACT_RELU) return z > 0.0f ? z : 0.0f;
+  if (act == SMOE_ACT_IDENTITY) return z;
   return __fdividef(z, 1.0f + __expf(-z));
 }
 
@@ -82,6 +85,7 @@ __device__ __forceinline__ float act_grad_fast(int act, float z) {
     return fmaf(z * 0.39894228040143268f, r.gexp, 0.5f * (1.0f + r.erf));
   }
   if (act == SMOE_ACT_RELU) return z > 0.0f ? 1.0f : 0.0f;
+  if (act == SMOE_ACT_IDENTITY) return 1.0f;
   const float s = __fdividef(1.0f, 1.0f + __expf(-z));
   return s * (1.0f + z * (1.0f - s));
 }

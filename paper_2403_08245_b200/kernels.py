@@ -386,6 +386,8 @@ def scatter2scatter_scaled(
     """scatter2scatter with a routing-weight-scaled activation epilogue (bf16, tcgen05).
 
     act_out given: out = x @ W (pre-activation), act_out = s * act(out);
+    activation="identity" (act = z, act' = 1) serves a plain routed linear with
+    combine weights (parallel_linear.backward's dp-in-epilogue path);
     act_grad_of given: out = s * (x @ W) * act'(act_grad_of) and, when
     dp_partials ([n, dp_parts(d_out)] fp32) is given, the per-row partial dot
     products sum(acc * act(act_grad_of)) for the combine-weight gradient.
@@ -393,8 +395,9 @@ def scatter2scatter_scaled(
     """
     if (act_out is None) == (act_grad_of is None):
         raise ValueError("give exactly one of act_out / act_grad_of")
-    if activation not in _lib.ACTIVATION_IDS:
+    if activation != "identity" and activation not in _lib.ACTIVATION_IDS:
         raise ValueError(f"unknown activation {activation!r}; choose from {sorted(_lib.ACTIVATION_IDS)}")
+    act_id = _lib.ACT_IDENTITY if activation == "identity" else _lib.ACTIVATION_IDS[activation]
     if x.dtype != torch.bfloat16:
         raise ValueError("scaled epilogues run on the bf16 tensor-core engine")
     num_slots = order.num_slots
@@ -416,7 +419,7 @@ def scatter2scatter_scaled(
     st = _lib.load().smoe_scatter2scatter_scaled(
         x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], w.shape[1], w.shape[2], order.o.data_ptr(),
         order.bin_offsets.data_ptr(), num_slots, fan_out, int(layout.grouped_in), int(layout.grouped_out),
-        int(transpose_w), epi, _lib.ACTIVATION_IDS[activation], scale.data_ptr(), out.data_ptr(), _ptr(act_out),
+        int(transpose_w), epi, act_id, scale.data_ptr(), out.data_ptr(), _ptr(act_out),
         _ptr(aux), _ptr(dp_partials), parts, _stream(x))
     _lt.end(_s2s_label(layout, transpose_w, _lib.EPI_ACT if act_out is not None else _lib.EPI_ACT_GRAD) + " scaled",
             t0)

@@ -97,3 +97,42 @@ def test_inference_combine_equals_training():
     y_inf, ctx = sm.parallel_linear_forward(x, w, order, p=p, fan_out=fan, layout=layout, training=False)
     assert ctx is None
     np.testing.assert_allclose(np_of(y_inf), np_of(y_train), rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("shape", [(512, 4, 16, 512, 2048), (300, 2, 8, 136, 264), (64, 3, 5, 72, 520)])
+def test_dp_epilogue_backward_bf16(shape, monkeypatch):
+    """bf16 backward with combine weights and a scattered fan-out-1 input (the
+    MoMHA output projection, moe_layers.py:446-449): dp computed inside the
+    input-gradient GEMM's epilogue (<dY W^T, x> partials) and p moved to the x
+    side of dW.  Against the oracle (bf16-rounded inputs, f64 accumulation) at
+    the bf16 bar, and against the reference-ordered path (combine_grad_p)."""
+    from oracle import scattermlp_oracle as orc
+    from gpu_util import bf16_round
+    t_tok, k, e, d_in, d_out = shape
+    rng = np.random.default_rng(sum(shape))
+    idx = np.stack([rng.permutation(e - 1)[:k] for _ in range(t_tok)])      # expert e-1 empty
+    p = rng.uniform(0.05, 1.0, (t_tok, k)).astype(np.float32)
+    n = t_tok * k
+    x = bf16_round(rng.uniform(-1, 1, (n, d_in)))
+    w = bf16_round(rng.uniform(-1, 1, (e, d_in, d_out)) / np.sqrt(d_in))
+    dy = bf16_round(rng.uniform(-1, 1, (t_tok, d_out)))
+    o, off = orc.compute_grouped_order(idx, e)
+    want_y, y_hat = orc.pl_forward(x.astype(np.float64), w.astype(np.float64), o, off, p.astype(np.float64), 1,
+                                   False, False)
+    want = orc.pl_backward(x.astype(np.float64), w.astype(np.float64), o, off, p.astype(np.float64), 1, False,
+                           False, y_hat, dy.astype(np.float64))
+    import sys
+    plmod = sys.modules["paper_2403_08245_b200.parallel_linear"]   # sm.parallel_linear is the function
+    order = order_of(idx, e)
+    got = {}
+    for mode in (True, False):
+        monkeypatch.setattr(plmod, "_DP_EPILOGUE", mode)
+        y, ctx = sm.parallel_linear_forward(t(x, torch.bfloat16), t(w, torch.bfloat16), order, p=t(p), fan_out=1,
+                                            layout=sm.SCATTERED_TO_SCATTERED)
+        gr = sm.parallel_linear_backward(ctx, t(dy, torch.bfloat16))
+        got[mode] = gr
+        assert rel_err(y, want_y) <= 2e-2
+        for val, ref, name in ((gr.dx, want[0], "dx"), (gr.dw, want[1], "dw"), (gr.dp, want[2], "dp")):
+            assert rel_err(val, ref) <= 2e-2, (mode, name, rel_err(val, ref))
+        assert float(gr.dw[e - 1].float().abs().max()) == 0.0
+    assert rel_err(got[True].dp, np_of(got[False].dp)) <= 1e-2
