@@ -363,6 +363,9 @@ def init_momha_weights(config: MomhaConfig, seed: int, dtype=torch.float32, devi
     )
 
 
+_GQA = os.environ.get("SMOE_MOMHA_GQA", "1") != "0"
+
+
 def _attn_core(q, keys, values, seq_len, d_head, k, causal):
     """Slot queries (T*k, d_proj) in chronological order vs dense K/V (T, d_proj).
 
@@ -377,9 +380,14 @@ def _attn_core(q, keys, values, seq_len, d_head, k, causal):
     b = n // seq_len
     h = q.shape[1] // d_head
     qh = q.view(b, seq_len, k, h, d_head).permute(0, 3, 2, 1, 4).reshape(b, h * k, seq_len, d_head)
-    kh = keys.view(b, seq_len, h, d_head).transpose(1, 2).repeat_interleave(k, dim=1)
-    vh = values.view(b, seq_len, h, d_head).transpose(1, 2).repeat_interleave(k, dim=1)
-    out = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=causal)
+    kh = keys.view(b, seq_len, h, d_head).transpose(1, 2)
+    vh = values.view(b, seq_len, h, d_head).transpose(1, 2)
+    if _GQA:
+        # K/V head hh serves query heads hh*k .. hh*k+k-1 without materialising k copies
+        out = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=causal, enable_gqa=k > 1)
+    else:
+        out = torch.nn.functional.scaled_dot_product_attention(qh, kh.repeat_interleave(k, dim=1),
+                                                               vh.repeat_interleave(k, dim=1), is_causal=causal)
     return out.view(b, h, k, seq_len, d_head).permute(0, 3, 2, 1, 4).reshape(b * seq_len * k, h * d_head)
 
 
