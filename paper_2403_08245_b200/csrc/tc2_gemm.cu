@@ -1137,7 +1137,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
-    if (epi != EPI_COMBINE && !peer_out && wide_for(d_in, epi)) {
+    if (!peer_out && wide_for(d_in, epi)) {
       const int64_t wide_tiles = ((n + 2 * TM - 1) / (2 * TM) + E) * ((d_out + TN - 1) / TN);
       p.group_m = (p.group_m + 1) / 2;  // bands in 512-row blocks
       p.wide_defer = wide_defer();
