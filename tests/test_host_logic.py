@@ -114,3 +114,30 @@ def test_mac_counter_is_padding_free_arithmetic():
     sm.add_macs(7)
     assert sm.mac_count() == 7
     sm.reset_mac_count()
+
+
+def test_bench_reference_arm_json_line():
+    """bench.py --impl reference (the oracle port on the host CPU) prints the
+    contract's JSON line: metric/unit/higher_is_better, impl, cpu_baseline and
+    an e2e object with zero transfer bytes; under torchrun only rank 0 prints."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "C0",
+                          "--steps", "1", "--warmup", "0", "--ref-tokens", "16"],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    env = dict(__import__("os").environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    out1 = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "C0",
+                           "--steps", "1", "--warmup", "0", "--ref-tokens", "16"],
+                          capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out1.returncode == 0 and not [ln for ln in out1.stdout.splitlines() if ln.startswith("{")]
