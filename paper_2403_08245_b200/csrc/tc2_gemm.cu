@@ -11,6 +11,11 @@
 //   * each CTA's epilogue drains its own TMEM rows.
 // Halving the B bytes each SM stages and reads per MMA is what lets the tensor
 // pipe run at full rate (SURVEY.md §7 "2-CTA 256-row tiles").
+// WIDE variant (template flag): 512 x 256 pair tiles — each CTA stages 256 A
+// rows as two 128-row halves next to its 128 B columns, and the leader issues
+// two M=256 MMAs per K16 step (rows m0.. into TMEM columns [0,256), rows
+// m0+256.. into [256,512)), cutting operand bytes per FLOP to 3/4; see
+// wide_stages() for why, and the grouped issue order in the MMA warp.
 //
 // Synchronisation (mbarriers; "L" = leader only):
 //   lfull[s]  per CTA: its own TMA bytes (+128 cp.async gather arrivals) landed.
@@ -20,8 +25,8 @@
 //             complete_tx lands on the leader's lfull.
 //             Weight-gradient K tails are zeroed by the leader in both CTAs.
 //   empty[s]  per CTA: the leader's MMAs consumed stage s (multicast commit)
-//   tfull[a]  per CTA: accumulator a complete (multicast commit)
-//   tempty[a] L: both CTAs' epilogues drained accumulator a (16 arrivals)
+//   tfull[a]  per CTA: accumulator a complete (multicast commit); WIDE: a = half
+//   tempty[a] L: both CTAs' epilogues drained accumulator a (16 arrivals); WIDE: a = half
 #include <atomic>
 
 #include "tc_common.cuh"
