@@ -15,6 +15,19 @@ namespace smoe {
 constexpr int kRowThreads = 256;
 constexpr int kRowWarps = kRowThreads / 32;
 
+// Launch `launch` (which names the template constant FKC) with the fan-out as
+// a compile-time constant for the common k = 1, 2, 4, 8, dynamic otherwise.
+#define SMOE_FANOUT_DISPATCH(fan, launch)       \
+  do {                                          \
+    switch (fan) {                              \
+      case 1: { constexpr int FKC = 1; launch; } break; \
+      case 2: { constexpr int FKC = 2; launch; } break; \
+      case 4: { constexpr int FKC = 4; launch; } break; \
+      case 8: { constexpr int FKC = 8; launch; } break; \
+      default: { constexpr int FKC = 0; launch; } break; \
+    }                                           \
+  } while (0)
+
 template <typename T> struct alignas(16) Vec {
   static constexpr int N = 16 / sizeof(T);
   T v[N];
@@ -70,7 +83,9 @@ __global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict_
 // and writes it (times w[s]) to the k grouped positions inv[s], s = t*F + j.
 // group_kernel's grouped-order visit re-reads each source row once per bin
 // (k times, from DRAM when x exceeds L2); this reads it once.
-template <typename T, bool VEC>
+// FK > 0: the fan-out is a compile-time constant (1, 2, 4, 8: destinations and
+// weights stay in registers and the k stores of a chunk issue back to back).
+template <typename T, bool VEC, int FK>
 __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restrict__ x, int64_t d,
                                                                 const int32_t *__restrict__ inv, int64_t t_rows,
                                                                 int fan_out, const float *__restrict__ weights,
@@ -79,11 +94,13 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
   const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (t >= t_rows) return;
   const T *src = x + t * d;
-  constexpr int MAXF = 16;
+  constexpr int MAXF = FK > 0 ? FK : 16;
   int64_t dst[MAXF];
   float wgt[MAXF];
-  const int F = fan_out < MAXF ? fan_out : MAXF;
-  for (int j = 0; j < F; ++j) {
+  const int F = FK > 0 ? FK : (fan_out < MAXF ? fan_out : MAXF);
+#pragma unroll
+  for (int j = 0; j < MAXF; ++j) {
+    if (j >= F) break;
     const int64_t s = t * fan_out + j;
     dst[j] = (int64_t)inv[s] * d;
     wgt[j] = weights ? weights[s] : 1.0f;
@@ -92,7 +109,9 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
       const Vec<T> v = ldv(src + c);
-      for (int j = 0; j < F; ++j) {
+#pragma unroll
+      for (int j = 0; j < MAXF; ++j) {
+        if (j >= F) break;
         Vec<T> o = v;
         if (weights) {
 #pragma unroll
@@ -104,7 +123,11 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
   } else {
     for (int64_t c = lane; c < d; c += 32) {
       const T v = src[c];
-      for (int j = 0; j < F; ++j) out[dst[j] + c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt[j]) : v;
+#pragma unroll
+      for (int j = 0; j < MAXF; ++j) {
+        if (j >= F) break;
+        out[dst[j] + c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt[j]) : v;
+      }
     }
   }
 }
@@ -177,14 +200,15 @@ __global__ void __launch_bounds__(kRowThreads) combine_grad_p_kernel(const T *__
 }
 
 // ---- fan-out reduce --------------------------------------------------------
-template <typename T, bool VEC>
+template <typename T, bool VEC, int FK>
 __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__restrict__ g,
-                                                                     int64_t Trows, int F,
+                                                                     int64_t Trows, int F_,
                                                                      int64_t d,
                                                                      T *__restrict__ dx) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (t >= Trows) return;
+  const int F = FK > 0 ? FK : F_;   // FK > 0: compile-time fan-out, all k loads in flight
   const T *src = g + t * F * d;
   T *dst = dx + t * d;
   if (VEC) {
@@ -193,7 +217,8 @@ __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__r
       float acc[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) acc[q] = 0.f;
-      for (int j = 0; j < F; ++j) {
+#pragma unroll
+      for (int j = 0; j < (FK > 0 ? FK : F); ++j) {
         Vec<T> v = ldv(src + (int64_t)j * d + c);
 #pragma unroll
         for (int q = 0; q < N; ++q) acc[q] += Num<T>::to_f(v.v[q]);
@@ -251,19 +276,19 @@ int group_inv(const void *x, int64_t t_rows, int64_t d, const int32_t *inv, int 
   if (dtype == SMOE_BF16) {
     using T = __nv_bfloat16;
     if (vec_ok(x, d, 2) && vec_ok(out, d, 2))
-      group_inv_kernel<T, true><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out, w,
-                                                                             (T *)out);
+      SMOE_FANOUT_DISPATCH(fan_out, (group_inv_kernel<T, true, FKC><<<row_blocks(t_rows), kRowThreads, 0, st>>>(
+                                        (const T *)x, d, inv, t_rows, fan_out, w, (T *)out)));
     else
-      group_inv_kernel<T, false><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
-                                                                              w, (T *)out);
+      group_inv_kernel<T, false, 0><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
+                                                                                 w, (T *)out);
   } else {
     using T = float;
     if (vec_ok(x, d, 4) && vec_ok(out, d, 4))
-      group_inv_kernel<T, true><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out, w,
-                                                                             (T *)out);
+      SMOE_FANOUT_DISPATCH(fan_out, (group_inv_kernel<T, true, FKC><<<row_blocks(t_rows), kRowThreads, 0, st>>>(
+                                        (const T *)x, d, inv, t_rows, fan_out, w, (T *)out)));
     else
-      group_inv_kernel<T, false><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
-                                                                              w, (T *)out);
+      group_inv_kernel<T, false, 0><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
+                                                                                 w, (T *)out);
   }
   return check_launch("group_inv");
 }
@@ -330,15 +355,17 @@ int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, voi
   if (dtype == SMOE_BF16) {
     using T = __nv_bfloat16;
     if (vec_ok(g, d, 2) && vec_ok(dx, d, 2))
-      fanout_reduce_kernel<T, true><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+      SMOE_FANOUT_DISPATCH(F, (fanout_reduce_kernel<T, true, FKC><<<row_blocks(Trows), kRowThreads, 0, st>>>(
+                                  (const T *)g, Trows, F, d, (T *)dx)));
     else
-      fanout_reduce_kernel<T, false><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+      fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
   } else {
     using T = float;
     if (vec_ok(g, d, 4) && vec_ok(dx, d, 4))
-      fanout_reduce_kernel<T, true><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+      SMOE_FANOUT_DISPATCH(F, (fanout_reduce_kernel<T, true, FKC><<<row_blocks(Trows), kRowThreads, 0, st>>>(
+                                  (const T *)g, Trows, F, d, (T *)dx)));
     else
-      fanout_reduce_kernel<T, false><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+      fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
   }
   return check_launch("fanout_reduce");
 }
