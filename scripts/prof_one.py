@@ -10,7 +10,9 @@ import paper_2403_08245_b200 as sm  # noqa: E402
 which = sys.argv[1]
 import os  # noqa: E402
 # SMOE_PROF_CFG=C2: the fine-grained config (E=64, k=8, d_expert=1792); default C1
-T, d, de, E, k = (32768, 4096, 1792, 64, 8) if os.environ.get("SMOE_PROF_CFG") == "C2" else (32768, 4096, 14336, 8, 2)
+# SMOE_PROF_CFG=C3: the MoMHA projections (d_model=2048, d_proj=512, E=16, k=4)
+_CFGS = {"C2": (32768, 4096, 1792, 64, 8), "C3": (32768, 2048, 512, 16, 4)}
+T, d, de, E, k = _CFGS.get(os.environ.get("SMOE_PROF_CFG", ""), (32768, 4096, 14336, 8, 2))
 n = T * k
 dev = "cuda"
 g = torch.Generator(device=dev).manual_seed(0)
@@ -70,6 +72,8 @@ for _ in range(3):
         sm.kernels.scatter2scatter_scaled(xg, w.view(E, de, d), order, 1, sm.GROUPED_TO_GROUPED, row_scale=pf,
                                           activation="gelu", out=h2, act_grad_of=h, dp_partials=parts,
                                           transpose_w=True)
+    elif which == "ofwd":  # scattered fan-out-1 input, scattered output, K = d_expert (C3 o-projection forward)
+        sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.SCATTERED_TO_SCATTERED, out=xg)
     elif which == "l2":
         sm.scatter2scatter(h, w.view(E, de, d), order, 1, sm.GROUPED_TO_SCATTERED, out=xg)
 torch.cuda.synchronize()
