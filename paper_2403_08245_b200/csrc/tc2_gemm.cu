@@ -193,9 +193,12 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     mbar_wait_acq_cluster(smem_u32(&ring_full[slot]), (uint32_t)(it / RING) & 1u);
     const int32_t t = *(volatile int32_t *)&s_tile[slot];
     __syncwarp();
-    if (elect_one_sync()) {
+    // The arrive only tells the leader the slot may be rewritten.  It is relaxed
+    // (a cluster-scope release would first drain this warp's global stores —
+    // the epilogue's previous tile); the branch on t orders it after the load.
+    if (elect_one_sync() && t != INT32_MIN) {
       if (leader) mbar_arrive(smem_u32(&ring_empty[slot]));
-      else mbar_arrive_release_cluster(smem_u32(&ring_empty[slot]), 0);
+      else mbar_arrive_relaxed_cluster(smem_u32(&ring_empty[slot]), 0);
     }
     return t;
   };

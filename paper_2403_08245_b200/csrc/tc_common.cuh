@@ -205,6 +205,17 @@ __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t local_bar, 
       "r"(cta)
       : "memory");
 }
+// relaxed arrive (cluster scope) on the barrier at this offset in CTA `cta`: no
+// ordering of this thread's earlier memory operations (a release arrive costs
+// MEMBAR.GPU + ERRBAR, i.e. waits for every outstanding global store)
+__device__ __forceinline__ void mbar_arrive_relaxed_cluster(uint32_t local_bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(local_bar),
+      "r"(cta)
+      : "memory");
+}
 // 32-bit store into the same shared offset of CTA `cta`
 __device__ __forceinline__ void st_cluster_u32(uint32_t local_addr, uint32_t cta, uint32_t v) {
   asm volatile(
