@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
   // band's L2 reuse into DRAM re-reads.
   auto next_tile = [&](int it) -> int64_t {  // ring reader (whole warp)
     const int slot = it & (RING - 1);
-    mbar_wait_acq_cluster(smem_u32(&ring_full[slot]), (uint32_t)(it / RING) & 1u);
+    // the peer's copy of the id arrives by a remote store: cluster-scope acquire
+    // (an L1 invalidation); the leader's own readers only need the CTA scope
+    if (leader) mbar_wait(smem_u32(&ring_full[slot]), (uint32_t)(it / RING) & 1u);
+    else mbar_wait_acq_cluster(smem_u32(&ring_full[slot]), (uint32_t)(it / RING) & 1u);
     const int32_t t = *(volatile int32_t *)&s_tile[slot];
     __syncwarp();
     // The arrive only tells the leader the slot may be rewritten.  It is relaxed
