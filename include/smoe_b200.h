@@ -127,6 +127,15 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
  * x[s / fan_out] * (weights ? weights[s] : 1) for every slot s (fan_out <= 16;
  * inverse = the grouped position of each slot, from smoe_route_sort).  Each
  * source row is read once instead of once per expert bin. */
+/* MoMHA query gradient in grouped order (the query projection's backward,
+ * moe_layers.py:468-473 + parallel_linear.py:208-222): row i of out is the slot
+ * s = order[i] (token t = s / k, choice j = s % k) read from the attention
+ * core's head layout heads[batch][hh * k + j][t % seq_len][0:d_head] for
+ * hh = 0 .. heads_per_slot - 1, i.e. out[i] = the slot's d_proj-wide row.  One
+ * pass replaces the head->slot permute and the grouped copy of the slot rows. */
+int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
+                          int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream);
+
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
                    const float *weights, int32_t dtype, void *out, void *stream);
 

@@ -33,6 +33,8 @@ int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, float
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
 int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const float *, int, void *, cudaStream_t);
+int heads_to_grouped(const void *, int64_t, int64_t, int, int, int, const int32_t *, int64_t, int, void *,
+                     cudaStream_t);
 int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
                               const int32_t *, int64_t, int, int, int, int, int, int, const float *, void *, void *,
                               const void *, float *, int, cudaStream_t);
@@ -190,6 +192,17 @@ int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, i
   if (n == 0) return SMOE_OK;
   REQUIRE(x && order && out, SMOE_EINVAL, "group: null pointer");
   return group(x, d, order, n, fan_out, weights, dtype, out, S(stream));
+}
+
+int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
+                          int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream) {
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  REQUIRE(batch >= 0 && seq_len >= 1 && k >= 1 && heads_per_slot >= 1 && d_head >= 1, SMOE_EINVAL,
+          "heads_to_grouped: bad dimensions");
+  REQUIRE(n == batch * seq_len * k, SMOE_ESHAPE, "heads_to_grouped: n must equal batch * seq_len * k");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(heads && order && out, SMOE_EINVAL, "heads_to_grouped: null pointer");
+  return heads_to_grouped(heads, batch, seq_len, k, heads_per_slot, d_head, order, n, dtype, out, S(stream));
 }
 
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,

@@ -132,6 +132,49 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
   }
 }
 
+// ---- MoMHA: attention-core head layout -> grouped slot rows ----------------
+// One warp per grouped row i: slot s = order[i], token t = s / k, choice j;
+// the row's d_proj = h * d_head values come from head hh * k + j of t's
+// sequence position, d_head contiguous elements per head (16-byte chunks).
+template <typename T>
+__global__ void __launch_bounds__(kRowThreads) heads_to_grouped_kernel(const T *__restrict__ heads, int64_t seq_len,
+                                                                       int k, int h, int dh,
+                                                                       const int32_t *__restrict__ order, int64_t n,
+                                                                       T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int64_t s = order[i];
+  const int64_t t = s / k;
+  const int j = (int)(s - t * k);
+  const int64_t b = t / seq_len, pos = t - b * seq_len;
+  constexpr int N = 16 / sizeof(T);           // elements per 16-byte chunk
+  const int cph = dh / N;                     // chunks per head
+  T *dst = out + i * (int64_t)h * dh;
+  for (int c = lane; c < h * cph; c += 32) {
+    const int hh = c / cph, q = c - hh * cph;
+    const T *src = heads + (((b * h + hh) * k + j) * seq_len + pos) * (int64_t)dh + q * N;
+    *reinterpret_cast<uint4 *>(dst + hh * dh + q * N) = __ldg(reinterpret_cast<const uint4 *>(src));
+  }
+}
+
+static inline unsigned row_blocks(int64_t rows);
+
+int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, int h, int dh, const int32_t *order,
+                     int64_t n, int dtype, void *out, cudaStream_t st) {
+  (void)batch;
+  const int esz = dtype == SMOE_BF16 ? 2 : 4;
+  if ((dh * esz) % 16 || (reinterpret_cast<uintptr_t>(heads) | reinterpret_cast<uintptr_t>(out)) % 16)
+    return fail(SMOE_ENOTSUP, "heads_to_grouped: d_head * element size must be a multiple of 16 bytes (aligned)");
+  if (dtype == SMOE_BF16)
+    heads_to_grouped_kernel<__nv_bfloat16><<<row_blocks(n), kRowThreads, 0, st>>>(
+        (const __nv_bfloat16 *)heads, seq_len, k, h, dh, order, n, (__nv_bfloat16 *)out);
+  else
+    heads_to_grouped_kernel<float><<<row_blocks(n), kRowThreads, 0, st>>>((const float *)heads, seq_len, k, h, dh,
+                                                                         order, n, (float *)out);
+  return check_launch("heads_to_grouped");
+}
+
 // ---- combine ---------------------------------------------------------------
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,

@@ -428,6 +428,29 @@ def scatter2scatter_scaled(
     return out
 
 
+def heads_to_grouped(heads: torch.Tensor, order: GroupedOrder, k: int) -> torch.Tensor:
+    """(n, h*d_head) slot rows in grouped order from the attention core's head layout.
+
+    heads: (batch, h*k, seq_len, d_head) contiguous, head hh*k + j = choice j's head hh
+    (moe_layers._attn_core); row i of the result is slot order.o[i]'s d_proj-wide row.
+    """
+    if heads.dim() != 4 or not heads.is_contiguous():
+        raise ValueError("heads must be a contiguous (batch, heads, seq_len, d_head) tensor")
+    b, hk, seq_len, dh = heads.shape
+    if hk % k:
+        raise ValueError(f"head count {hk} is not divisible by k={k}")
+    n = order.num_slots
+    require_dims(n == b * seq_len * k, "slots vs batch*seq_len*k", (n,), (b * seq_len * k,))
+    heads = _cuda(heads, "heads")
+    out = torch.empty((n, (hk // k) * dh), dtype=heads.dtype, device=heads.device)
+    t0 = _lt.begin()
+    st = _lib.load().smoe_heads_to_grouped(heads.data_ptr(), b, seq_len, k, hk // k, dh, order.o.data_ptr(), n,
+                                           _dtype_id(heads), out.data_ptr(), _stream(heads))
+    _lt.end("heads_to_grouped", t0)
+    _lib.check(st, "heads_to_grouped")
+    return out
+
+
 def dp_parts(d_out: int) -> int:
     return int(_lib.load().smoe_dp_parts(d_out))
 

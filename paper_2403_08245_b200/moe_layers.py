@@ -364,6 +364,7 @@ def init_momha_weights(config: MomhaConfig, seed: int, dtype=torch.float32, devi
 
 
 _GQA = os.environ.get("SMOE_MOMHA_GQA", "1") != "0"
+_GROUPED_DQ = os.environ.get("SMOE_MOMHA_GROUPED_DQ", "1") != "0"
 
 
 def _contig16(t: torch.Tensor) -> torch.Tensor:
@@ -519,7 +520,14 @@ def momha_backward(ctx: MomhaContext, dy, *, tile: TileConfig | None = None, led
         ctx.attn_graph = None
         d_out = _contig16(g_o.dx.to(out.dtype).view(b, sl, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, sl, dh)
         dqh, dkh, dvh = torch.autograd.grad(out, (qv, kv, vv), d_out)
-        dq = _contig16(dqh.view(b, h, kk, sl, dh).permute(0, 3, 2, 1, 4)).view(b * sl * kk, h * dh)
+        if _GROUPED_DQ and dqh.is_contiguous() and (dh * dqh.element_size()) % 16 == 0:
+            # the query gradient goes straight from the head layout to grouped
+            # rows: the query projection's backward then reads it by TMA (no
+            # gathers, parallel_linear.py:208-222 with a grouped dY)
+            dq = K.heads_to_grouped(dqh, ctx.query_ctx.order, kk)
+            ctx.query_ctx.y_was_grouped = True
+        else:
+            dq = _contig16(dqh.view(b, h, kk, sl, dh).permute(0, 3, 2, 1, 4)).view(b * sl * kk, h * dh)
         dk = _contig16(dkh.transpose(1, 2)).view(b * sl, h * dh)
         dv = _contig16(dvh.transpose(1, 2)).view(b * sl, h * dh)
     else:

@@ -56,3 +56,20 @@ def test_momha_bf16_matches_fp32_path():
     g16, g32 = sm.momha_backward(c16, dy), sm.momha_backward(c32, dy.float())
     for name in ("dx", "dwq", "dwk", "dwv", "dwo", "dp"):
         assert rel_err(getattr(g16, name), getattr(g32, name).cpu().numpy()) <= 2e-2, name
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_heads_to_grouped_matches_permute_and_group(dtype):
+    """smoe_heads_to_grouped == (head layout -> slot rows) then group() by the order."""
+    b, seq, k, h, dh, e = 3, 40, 4, 2, 64, 6
+    g = torch.Generator(device="cuda").manual_seed(9)
+    heads = torch.randn((b, h * k, seq, dh), device="cuda", generator=g).to(dtype)
+    t = b * seq
+    ids = torch.stack([torch.randperm(e, generator=torch.Generator().manual_seed(i))[:k] for i in range(t)]).cuda()
+    routing = sm.RoutingResult(ids, torch.rand(t, k, device="cuda"), torch.zeros(t, e, device="cuda"),
+                               renormalized=False, validate=False)
+    order = sm.compute_grouped_order(routing)
+    slots = heads.view(b, h, k, seq, dh).permute(0, 3, 2, 1, 4).reshape(t * k, h * dh)
+    want = slots[order.o.long()]
+    got = sm.kernels.heads_to_grouped(heads, order, k)
+    assert torch.equal(got, want)
