@@ -176,14 +176,20 @@ int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, i
 }
 
 // ---- combine ---------------------------------------------------------------
-template <typename T, bool VEC>
+template <typename T, bool VEC, int JK>
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,
                                                                const float *__restrict__ p,
-                                                               int64_t S, int J, int64_t d,
+                                                               int64_t S, int J_, int64_t d,
                                                                T *__restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (s >= S) return;
+  const int J = JK > 0 ? JK : J_;   // JK > 0: compile-time k (weights in registers, all k loads in flight)
+  float pw[JK > 0 ? JK : 1];
+  if (JK > 0) {
+#pragma unroll
+    for (int j = 0; j < (JK > 0 ? JK : 1); ++j) pw[j] = p[s * J + j];
+  }
   const T *src = y_hat + s * J * d;
   T *dst = y + s * d;
   if (VEC) {
@@ -192,8 +198,9 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
       float acc[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) acc[q] = 0.f;
-      for (int j = 0; j < J; ++j) {
-        const float pj = p[s * J + j];
+#pragma unroll
+      for (int j = 0; j < (JK > 0 ? JK : J); ++j) {
+        const float pj = JK > 0 ? pw[j] : p[s * J + j];
         Vec<T> v = ldv(src + (int64_t)j * d + c);
 #pragma unroll
         for (int q = 0; q < N; ++q) acc[q] = fmaf(pj, Num<T>::to_f(v.v[q]), acc[q]);
@@ -342,15 +349,17 @@ int combine(const void *y_hat, const float *p, int64_t S, int J, int64_t d, int 
   if (dtype == SMOE_BF16) {
     using T = __nv_bfloat16;
     if (vec_ok(y_hat, d, 2) && vec_ok(y, d, 2))
-      combine_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+      SMOE_FANOUT_DISPATCH(J, (combine_kernel<T, true, FKC><<<row_blocks(S), kRowThreads, 0, st>>>(
+                                  (const T *)y_hat, p, S, J, d, (T *)y)));
     else
-      combine_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+      combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
   } else {
     using T = float;
     if (vec_ok(y_hat, d, 4) && vec_ok(y, d, 4))
-      combine_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+      SMOE_FANOUT_DISPATCH(J, (combine_kernel<T, true, FKC><<<row_blocks(S), kRowThreads, 0, st>>>(
+                                  (const T *)y_hat, p, S, J, d, (T *)y)));
     else
-      combine_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
+      combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
   }
   return check_launch("combine");
 }
