@@ -90,7 +90,12 @@ def load(path: str | os.PathLike | None = None):
         _load_error = f"{p} not found; run `python -m paper_2403_08245_b200.build` (no CPU fallback exists)"
         raise LibraryError(_load_error)
     lib = ctypes.CDLL(str(p))
+    # SMOE_LIB_ALLOW_MISSING=1: A/B runs against an older build (SMOE_LIB) that
+    # predates some entry points; those stay unbound and fail if called
+    allow_missing = bool(os.environ.get("SMOE_LIB")) and os.environ.get("SMOE_LIB_ALLOW_MISSING") == "1"
     for name, (res, args) in SIGNATURES.items():
+        if allow_missing and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
