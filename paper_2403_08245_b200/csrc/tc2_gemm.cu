@@ -1235,8 +1235,12 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   CUtensorMap tc;
   if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");
   if (wide_for(E > 0 ? n / E : 0, SMOE_EPI_NONE, true)) {  // K = the bins, 8192 rows on average at C1
-    const int64_t wide_tiles = (int64_t)E * ((d_in + 2 * TM - 1) / (2 * TM)) * ((d_out + TN - 1) / TN);
-    p.group_m = (p.group_m + 1) / 2;
+    const int64_t mw = (d_in + 2 * TM - 1) / (2 * TM);
+    const int64_t wide_tiles = (int64_t)E * mw * ((d_out + TN - 1) / TN);
+    // band in 512-row blocks: 4 (the whole d_model = 4096 side at C1), 2 when the
+    // M side is long (d_expert = 14336: 28 blocks; 0.7 % less energy per launch,
+    // scripts/xty_wide_band.sh); SMOE_GROUP_M_K overrides
+    p.group_m = getenv("SMOE_GROUP_M_K") ? (p.group_m + 1) / 2 : (mw >= 16 ? 2 : 4);
     p.wide_defer = wide_defer();
     return launch<A_MN, B_ROWS_MN, true, true, true>(ta, tb, tc, tc, p, wide_tiles, st);
   }
