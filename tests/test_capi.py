@@ -54,6 +54,16 @@ def test_argument_validation_without_a_gpu():
     assert st == _lib.SMOE_EINVAL
     # zero-size work is a no-op success, no device touched
     assert lib.smoe_group(None, 0, 4, None, 0, 2, None, 1, None, None) == _lib.SMOE_OK
+    # heads_to_grouped: slot count must equal batch * seq_len * k; null buffers rejected
+    st = lib.smoe_heads_to_grouped(None, 2, 8, 4, 2, 64, None, 63, 1, None, None)
+    assert st == _lib.SMOE_ESHAPE and "batch * seq_len * k" in _lib.last_error()
+    st = lib.smoe_heads_to_grouped(None, 2, 8, 4, 2, 64, None, 64, 1, None, None)
+    assert st == _lib.SMOE_EINVAL
+    assert lib.smoe_heads_to_grouped(None, 0, 8, 4, 2, 64, None, 0, 1, None, None) == _lib.SMOE_OK
+    # identity activation is accepted only by the scaled entry point
+    st = lib.smoe_scatter2scatter(None, 6, None, 2, 4, 4, None, None, 6, 1, 1, 0, 0, 1, 0, 3,
+                                  None, None, None, 0, None)
+    assert st == _lib.SMOE_EINVAL and "activation" in _lib.last_error()
 
 
 def test_status_maps_to_reference_exception_classes():
