@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SMOE_ABI_VERSION 2
+#define SMOE_ABI_VERSION 3
 
 typedef enum {
   SMOE_OK = 0,
@@ -43,7 +43,13 @@ typedef enum {
   SMOE_ENOTSUP = 4  /* valid but unsupported combination on this build        */
 } smoe_status;
 
-typedef enum { SMOE_F32 = 0, SMOE_BF16 = 1 } smoe_dtype;
+/* Storage dtypes.  bf16: tcgen05 tensor cores, fp32 accumulation (the product
+ * path).  F32: the check mode — SIMT kernels with 64-bit accumulation and one
+ * rounding, the reference's numeric contract (core_tensor.py:1-7).  F64: the
+ * reference's float64 verification dtype (its finite-difference gradient
+ * checks), SIMT only.  Per-slot weights (group weights, combine weights p) and
+ * dp are float32 except with SMOE_F64 storage, where they are float64. */
+typedef enum { SMOE_F32 = 0, SMOE_BF16 = 1, SMOE_F64 = 2 } smoe_dtype;
 
 /* Activations of moe_layers.py:42-72 (exact-erf GELU, ReLU, SiLU). */
 typedef enum { SMOE_ACT_GELU = 0, SMOE_ACT_RELU = 1, SMOE_ACT_SILU = 2,
@@ -63,8 +69,12 @@ typedef enum {
                                   sum over the part's columns of acc * act(aux)                */
 } smoe_epilogue;
 
-/* GEMM engine selection: AUTO picks tcgen05 for bf16 and the SIMT fp32 kernel
- * for the fp32 check mode. */
+/* GEMM engine selection: AUTO runs bf16 on tcgen05 and the fp32 / fp64 check
+ * modes on the SIMT kernels.  There is no silent fallback: a bf16 call the
+ * tcgen05 engine cannot take (d_in or d_out not a multiple of 8, a buffer not
+ * 16-byte aligned, more than 1024 experts, no sm_100a device) returns
+ * SMOE_ENOTSUP.  SMOE_ENGINE_SIMT runs bf16 on the SIMT kernels only when
+ * asked for explicitly (the tests' cross-check of the tcgen05 engine). */
 typedef enum { SMOE_ENGINE_AUTO = 0, SMOE_ENGINE_SIMT = 1, SMOE_ENGINE_TCGEN05 = 2 } smoe_engine;
 
 const char *smoe_get_last_error(void);
@@ -137,7 +147,7 @@ int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int
                           int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream);
 
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
-                   const float *weights, int32_t dtype, void *out, void *stream);
+                   const void *weights, int32_t dtype, void *out, void *stream);
 
 /* ---------------------------------------------------------------------------
  * group_xty (kernels.py:329-361): dw[e] = xg[bin e]^T @ yg[bin e]; empty bin -> 0.
@@ -149,20 +159,20 @@ int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets
 
 /* ---------------------------------------------------------------------------
  * group (kernels.py:289-326): out[i] = x[order[i] / fan_out] * (weights ? weights[order[i]] : 1)
- *   x [n / fan_out, d], weights [n] float32 or NULL, out [n, d]
+ *   x [n / fan_out, d], weights [n] float32 (float64 for SMOE_F64) or NULL, out [n, d].
  */
 int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, int64_t n,
-               int32_t fan_out, const float *weights, int32_t dtype, void *out, void *stream);
+               int32_t fan_out, const void *weights, int32_t dtype, void *out, void *stream);
 
 /* _combine (parallel_linear.py:69-73): y[s] = sum_j p[s,j] * y_hat[s*J + j]
- *   y_hat [S*J, d], p [S, J] float32, y [S, d]                            */
-int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_cols, int64_t d,
+ *   y_hat [S*J, d], p [S, J] float32 (float64 for SMOE_F64), y [S, d]     */
+int smoe_combine(const void *y_hat, const void *p, int64_t s_rows, int32_t j_cols, int64_t d,
                  int32_t dtype, void *y, void *stream);
 
 /* dp (parallel_linear.py:198-206): dp[s,j] = <dy[s], y_hat[s*J + j]>
- *   dy [S, d], y_hat [S*J, d], dp [S, J] float32                          */
+ *   dy [S, d], y_hat [S*J, d], dp [S, J] float32 (float64 for SMOE_F64)   */
 int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
-                        int64_t d, int32_t dtype, float *dp, void *stream);
+                        int64_t d, int32_t dtype, void *dp, void *stream);
 
 /* fan-out reduce (parallel_linear.py:259-266): dx[t] = sum_j g[t*F + j]
  *   g [T*F, d], dx [T, d]                                                 */
@@ -212,20 +222,23 @@ int smoe_group_xty_scattered(const void *x, int64_t x_rows, int32_t x_fan_out, i
 /* ---------------------------------------------------------------------------
  * scatter_combine (kernels.py:242-286), inference: y[order[i] / combine_cols] +=
  *   p_flat[order[i]] * (x[src] @ W[e]) with no T*k buffer.
- *   y_accum [n / combine_cols, d_out] float32, zeroed by this call.
+ *   p_flat  [n] float32 (float64 for SMOE_F64).
+ *   y_accum [n / combine_cols, d_out] float32, zeroed by this call (unused
+ *           for SMOE_F64, which accumulates in y itself).
  *   y       [n / combine_cols, d_out] dtype (rounded copy of y_accum; may be
  *           the same buffer as y_accum when dtype == SMOE_F32).
  *   engine  SMOE_ENGINE_AUTO: bf16 runs the tcgen05 CTA-pair GEMM whose
  *           epilogue scales each row by p and adds it into y_accum with fp32
  *           vector reductions (order of the k additions per token is not
  *           fixed: bit-reproducible for k <= 2, within fp32 rounding above);
- *           fp32 and unsupported shapes run the SIMT kernel.
+ *           shapes it cannot take return SMOE_ENOTSUP (no SIMT fallback for
+ *           bf16).  fp32 / fp64 run the SIMT check-mode kernel.
  */
 int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
                          int64_t d_in, int64_t d_out, const int32_t *order,
                          const int32_t *expert_offsets, int64_t n, int32_t fan_out,
-                         const float *p_flat, int32_t combine_cols, int32_t grouped_in,
-                         int32_t dtype, float *y_accum, void *y, int32_t engine, void *stream);
+                         const void *p_flat, int32_t combine_cols, int32_t grouped_in,
+                         int32_t dtype, void *y_accum, void *y, int32_t engine, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Expert parallelism over peer memory (the

@@ -12,7 +12,9 @@ paths are relative to /root/reference/pkg/src/scattermlp/):
   * routing order = stable argsort of the flattened ids + bincount + cumsum;
   * the four scatter2scatter layouts, scatter_combine, group, group_xty,
     the weighted combine and its dp, ParallelLinear forward / backward with
-    the buffer-reuse order, and the SMoE MLP forward / backward.
+    the buffer-reuse order, and the SMoE MLP forward / backward;
+  * the mixture-of-attention layer: slot-query attention and its backward,
+    momha_forward / momha_backward (moe_layers.py:270-482).
 
 Parity pinning: tests/golden/*.npz hold input/output vectors produced by
 importing the reference itself (tests/golden/make_golden.py, run in the
@@ -269,6 +271,107 @@ def naive_smoe_mlp(x, w1, w2, expert_idx, p, activation="gelu"):
             h = act(xt @ w1[e].astype(F64), activation).astype(F64)
             y[tok] += float(p[tok, sel]) * (h @ w2[e].astype(F64))
     return y.astype(x.dtype)
+
+
+# ---------------------------------------------------------------------------
+# Mixture of multi-head attention (moe_layers.py:270-482)
+
+
+def _causal_chunks(n_tokens, seq_len, k, chunk_slots=2048):
+    """(token lo, token hi, slot lo, slot hi) query chunks, never crossing a sequence."""
+    if n_tokens % seq_len:
+        raise ValueError(f"token count {n_tokens} is not divisible by seq_len {seq_len}")
+    for lo in range(0, n_tokens, seq_len):
+        for s0 in range(lo * k, (lo + seq_len) * k, chunk_slots):
+            yield lo, lo + seq_len, s0, min(s0 + chunk_slots, (lo + seq_len) * k)
+
+
+def attention(q, keys, values, k, seq_len, d_head, causal=True):
+    """Per-slot queries vs dense keys (moe_layers.py:280-327).
+
+    Slots are chronological (slot s belongs to token s // k, as momha_forward
+    lays them out, :441); query head columns [c0, c0 + d_head) attend with the
+    same columns of the keys / values of the slot's sequence, causally.  Scores
+    and softmax in f64, one rounding.  Query rows are processed in chunks so a
+    4096-token sequence stays within a few hundred MB.
+    """
+    n = keys.shape[0]
+    out = np.empty(q.shape, dtype=q.dtype)
+    scale = 1.0 / math.sqrt(d_head)
+    qd, kd, vd = q.astype(F64), keys.astype(F64), values.astype(F64)
+    for lo, hi, s0, s1 in _causal_chunks(n, seq_len, k):
+        times = np.arange(s0, s1) // k - lo
+        mask = times[:, None] < np.arange(hi - lo)[None, :] if causal else None
+        for c0 in range(0, q.shape[1], d_head):
+            c = slice(c0, c0 + d_head)
+            sc = (qd[s0:s1, c] @ kd[lo:hi, c].T) * scale
+            if mask is not None:
+                sc = np.where(mask, -np.inf, sc)
+            sc -= sc.max(axis=1, keepdims=True)
+            wts = np.exp(sc)
+            wts /= wts.sum(axis=1, keepdims=True)
+            out[s0:s1, c] = (wts @ vd[lo:hi, c]).astype(q.dtype)
+    return out
+
+
+def attention_backward(q, keys, values, k, seq_len, d_head, causal, d_out):
+    """(dq, dkeys, dvalues) with recomputed probabilities (moe_layers.py:330-377)."""
+    n = keys.shape[0]
+    scale = 1.0 / math.sqrt(d_head)
+    qd, kd, vd, god = q.astype(F64), keys.astype(F64), values.astype(F64), d_out.astype(F64)
+    dq = np.zeros_like(qd)
+    dk = np.zeros_like(kd)
+    dv = np.zeros_like(vd)
+    for lo, hi, s0, s1 in _causal_chunks(n, seq_len, k):
+        times = np.arange(s0, s1) // k - lo
+        mask = times[:, None] < np.arange(hi - lo)[None, :] if causal else None
+        for c0 in range(0, q.shape[1], d_head):
+            c = slice(c0, c0 + d_head)
+            sc = (qd[s0:s1, c] @ kd[lo:hi, c].T) * scale
+            if mask is not None:
+                sc = np.where(mask, -np.inf, sc)
+            sc -= sc.max(axis=1, keepdims=True)
+            pr = np.exp(sc)
+            pr /= pr.sum(axis=1, keepdims=True)
+            g = god[s0:s1, c]
+            dpr = g @ vd[lo:hi, c].T
+            ds = pr * (dpr - (dpr * pr).sum(axis=1, keepdims=True))
+            dq[s0:s1, c] = (ds @ kd[lo:hi, c]) * scale
+            dk[lo:hi, c] += (ds.T @ qd[s0:s1, c]) * scale
+            dv[lo:hi, c] += pr.T @ g
+    return dq.astype(q.dtype), dk.astype(q.dtype), dv.astype(q.dtype)
+
+
+def _matmul(a, b):
+    """core_tensor.matmul (core_tensor.py:130-143): f64 accumulation, one rounding."""
+    return (a.astype(F64) @ b.astype(F64)).astype(a.dtype)
+
+
+def momha_forward(x, wq, wk, wv, wo, expert_idx, p, num_experts, seq_len, d_head, causal=True):
+    """y and the saved state (moe_layers.py:406-457): dense K/V, routed Q / O projections."""
+    k = expert_idx.shape[1]
+    o, off = compute_grouped_order(expert_idx, num_experts)
+    keys, values = _matmul(x, wk), _matmul(x, wv)
+    q = scatter2scatter(x, wq, o, off, k, False, False)
+    attn = attention(q, keys, values, k, seq_len, d_head, causal)
+    y, y_hat = pl_forward(attn, wo, o, off, p, 1, False, False)
+    return y, dict(o=o, off=off, k=k, q=q, keys=keys, values=values, attn=attn, y_hat=y_hat,
+                   seq_len=seq_len, d_head=d_head, causal=causal)
+
+
+def momha_backward(x, wq, wk, wv, wo, p, state, dy):
+    """(dx, dwq, dwk, dwv, dwo, dp) (moe_layers.py:460-482)."""
+    o, off, k = state["o"], state["off"], state["k"]
+    dattn, dwo, dp = pl_backward(state["attn"], wo, o, off, p, 1, False, False, state["y_hat"], dy)
+    dq, dk, dv = attention_backward(state["q"], state["keys"], state["values"], k, state["seq_len"],
+                                    state["d_head"], state["causal"], dattn)
+    dx_q, dwq, _ = pl_backward(x, wq, o, off, None, k, False, False, None, dq)
+    x64 = x.astype(F64)
+    dwk = (x64.T @ dk.astype(F64)).astype(x.dtype)
+    dwv = (x64.T @ dv.astype(F64)).astype(x.dtype)
+    dx_kv = dk.astype(F64) @ wk.astype(F64).T + dv.astype(F64) @ wv.astype(F64).T
+    dx = (dx_q.astype(F64) + dx_kv).astype(x.dtype)
+    return dx, dwq, dwk, dwv, dwo, dp
 
 
 # ---------------------------------------------------------------------------

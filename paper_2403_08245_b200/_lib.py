@@ -14,12 +14,12 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-# SMOE_LIB overrides the in-tree library (used by scripts/ab.sh to A/B two builds
+# SMOE_LIB overrides the in-tree library (used by scripts/ab/ab.sh to A/B two builds
 # of the same C ABI inside one GPU session).
 LIB_PATH = Path(os.environ["SMOE_LIB"]) if os.environ.get("SMOE_LIB") else _PKG / "libsmoe_b200.so"
 
 SMOE_OK, SMOE_EINVAL, SMOE_ESHAPE, SMOE_ECUDA, SMOE_ENOTSUP = range(5)
-SMOE_F32, SMOE_BF16 = 0, 1
+SMOE_F32, SMOE_BF16, SMOE_F64 = 0, 1, 2
 ACTIVATION_IDS = {"gelu": 0, "relu": 1, "silu": 2}
 ACT_IDENTITY = 3   # scatter2scatter_scaled only (routed linear with combine weights)
 EPI_NONE, EPI_ACT, EPI_ACT_GRAD, EPI_ACT_ONLY, EPI_ACT_SCALED, EPI_ACT_GRAD_SCALED = 0, 1, 2, 3, 4, 5
@@ -77,7 +77,7 @@ class LibraryError(RuntimeError):
     """The native library is missing or a native call failed."""
 
 
-ABI_VERSION = 2  # include/smoe_b200.h SMOE_ABI_VERSION
+ABI_VERSION = 3  # include/smoe_b200.h SMOE_ABI_VERSION
 
 
 def load(path: str | os.PathLike | None = None):

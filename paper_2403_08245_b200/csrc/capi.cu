@@ -27,12 +27,12 @@ int check_launch(const char *what, int launches) {
 // engines (defined in the other translation units)
 size_t route_sort_workspace(int64_t n, int E);
 int route_sort(const int64_t *, int64_t, int, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
-int group(const void *, int64_t, const int32_t *, int64_t, int, const float *, int, void *, cudaStream_t);
-int combine(const void *, const float *, int64_t, int, int64_t, int, void *, cudaStream_t);
-int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, float *, cudaStream_t);
+int group(const void *, int64_t, const int32_t *, int64_t, int, const void *, int, void *, cudaStream_t);
+int combine(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
-int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const float *, int, void *, cudaStream_t);
+int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const void *, int, void *, cudaStream_t);
 int heads_to_grouped(const void *, int64_t, int64_t, int, int, int, const int32_t *, int64_t, int, void *,
                      cudaStream_t);
 int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
@@ -41,7 +41,8 @@ int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t,
 int activation(const void *, int64_t, int, int, int, void *, cudaStream_t);
 int simt_scatter2scatter(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int simt_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int, void *, cudaStream_t);
-int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, const float *, int, int, int, float *, void *, cudaStream_t);
+int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int,
+                         const void *, int, int, int, void *, void *, cudaStream_t);
 int router_topk(const float *, int64_t, int, int, int, int, float *, int64_t *, float *, cudaStream_t);
 int router_backward(const float *, const int64_t *, const float *, int64_t, int, int, int, float *, cudaStream_t);
 bool tc_available();
@@ -71,7 +72,7 @@ static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s)
 static inline std::string dims(int64_t a, int64_t b) {
   return "(" + std::to_string(a) + ", " + std::to_string(b) + ")";
 }
-static inline bool valid_dtype(int32_t d) { return d == SMOE_F32 || d == SMOE_BF16; }
+static inline bool valid_dtype(int32_t d) { return d == SMOE_F32 || d == SMOE_BF16 || d == SMOE_F64; }
 
 extern "C" {
 
@@ -129,9 +130,12 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
   REQUIRE(epilogue != SMOE_EPI_ACT_GRAD || aux, SMOE_EINVAL, "EPI_ACT_GRAD needs aux");
   REQUIRE(x && w && order && expert_offsets && out, SMOE_EINVAL, "scatter2scatter: null pointer");
   const int64_t d_in = transpose_w ? w_cols : w_rows, d_out = transpose_w ? w_rows : w_cols;
-  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
-                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && tc_supports_s2s(d_in, d_out, x, w, out));
+  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16);
   if (use_tc) {
+    REQUIRE(tc_available(), SMOE_ENOTSUP, "bf16 runs on the sm_100a tcgen05 engine only (no such device)");
+    REQUIRE(tc_supports_s2s(d_in, d_out, x, w, out), SMOE_ENOTSUP,
+            "bf16 scatter2scatter needs d_in, d_out multiples of 8 and 16-byte aligned buffers (got d_in=" +
+                std::to_string(d_in) + ", d_out=" + std::to_string(d_out) + "); there is no SIMT fallback");
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
     return tc_scatter2scatter(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
                               grouped_in, grouped_out, transpose_w, epilogue, activation, out, out2, aux, S(stream));
@@ -153,10 +157,14 @@ int smoe_group_xty_scattered(const void *x, int64_t x_rows, int32_t x_fan_out, i
           "x rows (" + std::to_string(x_rows) + ") do not cover the " + std::to_string(n) + " slots");
   REQUIRE(y_grouped ? y_rows == n : y_rows * y_fan_out == n, SMOE_ESHAPE,
           "y rows (" + std::to_string(y_rows) + ") do not cover the " + std::to_string(n) + " slots");
-  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
-                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && n > 0 &&
-                 tc_supports_xty_scattered(num_experts, x_rows, d_in, y_rows, d_out, x, y, dw));
+  if (n == 0) return simt_group_xty_scattered(x, x_fan_out, x_grouped, y, y_fan_out, y_grouped, order,
+                                              expert_offsets, num_experts, d_in, d_out, dtype, dw, S(stream));
+  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16);
   if (use_tc) {
+    REQUIRE(tc_available(), SMOE_ENOTSUP, "bf16 runs on the sm_100a tcgen05 engine only (no such device)");
+    REQUIRE(tc_supports_xty_scattered(num_experts, x_rows, d_in, y_rows, d_out, x, y, dw), SMOE_ENOTSUP,
+            "bf16 group_xty over scattered operands needs d_in, d_out multiples of 8, 16-byte aligned buffers and "
+            "at most 1024 experts; there is no SIMT fallback");
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
     return tc_group_xty_scattered(x, x_rows, x_fan_out, x_grouped, y, y_rows, y_fan_out, y_grouped, order,
                                   expert_offsets, num_experts, n, d_in, d_out, dw, S(stream));
@@ -172,10 +180,12 @@ int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets
   REQUIRE(num_experts >= 1, SMOE_EINVAL, "num_experts must be >= 1");
   REQUIRE(dw && expert_offsets, SMOE_EINVAL, "group_xty: null pointer");
   REQUIRE(n == 0 || (xg && yg), SMOE_EINVAL, "group_xty: null pointer");
-  bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
-                (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() && n > 0 &&
-                 tc_supports_s2s(d_in, d_out, xg, yg, dw));
+  if (n == 0) return simt_group_xty(xg, yg, expert_offsets, num_experts, d_in, d_out, dtype, dw, S(stream));
+  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16);
   if (use_tc) {
+    REQUIRE(tc_available(), SMOE_ENOTSUP, "bf16 runs on the sm_100a tcgen05 engine only (no such device)");
+    REQUIRE(tc_supports_s2s(d_in, d_out, xg, yg, dw), SMOE_ENOTSUP,
+            "bf16 group_xty needs d_in, d_out multiples of 8 and 16-byte aligned buffers; there is no SIMT fallback");
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only");
     return tc_group_xty(xg, yg, expert_offsets, num_experts, n, d_in, d_out, dw, S(stream));
   }
@@ -183,7 +193,7 @@ int smoe_group_xty(const void *xg, const void *yg, const int32_t *expert_offsets
 }
 
 int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, int64_t n,
-               int32_t fan_out, const float *weights, int32_t dtype, void *out, void *stream) {
+               int32_t fan_out, const void *weights, int32_t dtype, void *out, void *stream) {
   REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1, got " + std::to_string(fan_out));
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   REQUIRE(x_rows * fan_out == n, SMOE_EINVAL,
@@ -196,7 +206,7 @@ int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, i
 
 int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
                           int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream) {
-  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  REQUIRE(dtype == SMOE_F32 || dtype == SMOE_BF16, SMOE_EINVAL, "heads_to_grouped: bf16 or fp32 only");
   REQUIRE(batch >= 0 && seq_len >= 1 && k >= 1 && heads_per_slot >= 1 && d_head >= 1, SMOE_EINVAL,
           "heads_to_grouped: bad dimensions");
   REQUIRE(n == batch * seq_len * k, SMOE_ESHAPE, "heads_to_grouped: n must equal batch * seq_len * k");
@@ -206,7 +216,7 @@ int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int
 }
 
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
-                   const float *weights, int32_t dtype, void *out, void *stream) {
+                   const void *weights, int32_t dtype, void *out, void *stream) {
   REQUIRE(fan_out >= 1 && fan_out <= 16, SMOE_EINVAL, "group_inv: fan_out must be in [1, 16]");
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   if (x_rows == 0) return SMOE_OK;
@@ -214,7 +224,7 @@ int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inve
   return group_inv(x, x_rows, d, inverse, fan_out, weights, dtype, out, S(stream));
 }
 
-int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_cols, int64_t d,
+int smoe_combine(const void *y_hat, const void *p, int64_t s_rows, int32_t j_cols, int64_t d,
                  int32_t dtype, void *y, void *stream) {
   REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine: J must be >= 1");
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
@@ -224,7 +234,7 @@ int smoe_combine(const void *y_hat, const float *p, int64_t s_rows, int32_t j_co
 }
 
 int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
-                        int64_t d, int32_t dtype, float *dp, void *stream) {
+                        int64_t d, int32_t dtype, void *dp, void *stream) {
   REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine_grad_p: J must be >= 1");
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   if (s_rows == 0) return SMOE_OK;
@@ -289,8 +299,8 @@ int smoe_apply_activation(const void *x, int64_t numel, int32_t act, int32_t der
 int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t num_experts,
                          int64_t d_in, int64_t d_out, const int32_t *order,
                          const int32_t *expert_offsets, int64_t n, int32_t fan_out,
-                         const float *p_flat, int32_t combine_cols, int32_t grouped_in,
-                         int32_t dtype, float *y_accum, void *y, int32_t engine, void *stream) {
+                         const void *p_flat, int32_t combine_cols, int32_t grouped_in,
+                         int32_t dtype, void *y_accum, void *y, int32_t engine, void *stream) {
   REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
   REQUIRE(combine_cols >= 1 && n % combine_cols == 0, SMOE_EINVAL,
           "combine width " + std::to_string(combine_cols) + " must divide T*k (" + std::to_string(n) + ")");
@@ -300,20 +310,23 @@ int smoe_scatter_combine(const void *x, int64_t x_rows, const void *w, int32_t n
   else
     REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
   if (n == 0) return SMOE_OK;  // empty tensors may carry null pointers
+  if (dtype == SMOE_F64) y_accum = y;  // float64 storage accumulates in y itself
   REQUIRE(y_accum && y, SMOE_EINVAL, "scatter_combine: null output");
   if (d_out == 0) return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n,
                                                         fan_out, p_flat, combine_cols, grouped_in, dtype, y_accum, y,
                                                         S(stream));
   REQUIRE(x && w && order && expert_offsets && p_flat, SMOE_EINVAL, "scatter_combine: null pointer");
-  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 ||
-                      (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16 && tc_available() &&
-                       tc_supports_combine(num_experts, d_in, d_out, x, w, y_accum));
+  const bool use_tc = engine == SMOE_ENGINE_TCGEN05 || (engine == SMOE_ENGINE_AUTO && dtype == SMOE_BF16);
   if (use_tc) {
+    REQUIRE(tc_available(), SMOE_ENOTSUP, "bf16 runs on the sm_100a tcgen05 engine only (no such device)");
+    REQUIRE(tc_supports_combine(num_experts, d_in, d_out, x, w, (const void *)y_accum), SMOE_ENOTSUP,
+            "bf16 scatter_combine needs d_in, d_out multiples of 8, 16-byte aligned buffers and at most 1024 "
+            "experts; there is no SIMT fallback");
     REQUIRE(dtype == SMOE_BF16, SMOE_ENOTSUP, "tcgen05 engine is bf16-only (fp32 check mode runs on SIMT)");
     int st = tc_scatter_combine(x, x_rows, w, num_experts, d_in, d_out, order, expert_offsets, n, fan_out, grouped_in,
-                                p_flat, combine_cols, y_accum, S(stream));
+                                (const float *)p_flat, combine_cols, (float *)y_accum, S(stream));
     if (st != SMOE_OK) return st;
-    return round_copy(y_accum, (n / combine_cols) * d_out, dtype, y, S(stream));
+    return round_copy((const float *)y_accum, (n / combine_cols) * d_out, dtype, y, S(stream));
   }
   return simt_scatter_combine(x, w, num_experts, d_in, d_out, order, expert_offsets, n, fan_out, p_flat,
                               combine_cols, grouped_in, dtype, y_accum, y, S(stream));

@@ -1,6 +1,7 @@
 // HBM-bound row kernels of the ParallelLinear path (K5/K9 and the combine /
 // fan-out reductions of SURVEY.md §2.3).  One warp owns one output row and
-// moves it with 16-byte vectors; all sums are fp32 and written once, so the
+// moves it with 16-byte vectors; sums accumulate in fp32 for bf16 storage and
+// in 64-bit for the fp32 check mode, are rounded once and written once, so the
 // results are deterministic (no atomics anywhere).
 //
 //   group            kernels.py:289-326       out[i] = x[o[i]/F] * w[o[i]]
@@ -51,29 +52,31 @@ template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict__ x, int64_t d,
                                                              const int32_t *__restrict__ order,
                                                              int64_t n, int fan_out,
-                                                             const float *__restrict__ weights,
+                                                             const typename WOf<T>::type *__restrict__ weights,
                                                              T *__restrict__ out) {
+  using A = typename AccOf<T>::type;
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (i >= n) return;
   const int32_t slot = order[i];
   const T *src = x + (int64_t)(slot / fan_out) * d;
   T *dst = out + i * d;
-  const float wgt = weights ? weights[slot] : 1.0f;
+  // the product is rounded to the storage dtype (kernels.py:323-325)
+  const A wgt = weights ? (A)weights[slot] : A(1);
   if (VEC) {
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
       Vec<T> v = ldv(src + c);
       if (weights) {
 #pragma unroll
-        for (int q = 0; q < N; ++q) v.v[q] = Num<T>::from_f(Num<T>::to_f(v.v[q]) * wgt);
+        for (int q = 0; q < N; ++q) v.v[q] = Conv<T>::from_acc(Conv<T>::to_acc(v.v[q]) * wgt);
       }
       stv(dst + c, v);
     }
   } else {
     for (int64_t c = lane; c < d; c += 32) {
       T v = src[c];
-      dst[c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt) : v;
+      dst[c] = weights ? Conv<T>::from_acc(Conv<T>::to_acc(v) * wgt) : v;
     }
   }
 }
@@ -88,22 +91,24 @@ __global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict_
 template <typename T, bool VEC, int FK>
 __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restrict__ x, int64_t d,
                                                                 const int32_t *__restrict__ inv, int64_t t_rows,
-                                                                int fan_out, const float *__restrict__ weights,
+                                                                int fan_out,
+                                                                const typename WOf<T>::type *__restrict__ weights,
                                                                 T *__restrict__ out) {
+  using A = typename AccOf<T>::type;
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (t >= t_rows) return;
   const T *src = x + t * d;
   constexpr int MAXF = FK > 0 ? FK : 16;
   int64_t dst[MAXF];
-  float wgt[MAXF];
+  A wgt[MAXF];
   const int F = FK > 0 ? FK : (fan_out < MAXF ? fan_out : MAXF);
 #pragma unroll
   for (int j = 0; j < MAXF; ++j) {
     if (j >= F) break;
     const int64_t s = t * fan_out + j;
     dst[j] = (int64_t)inv[s] * d;
-    wgt[j] = weights ? weights[s] : 1.0f;
+    wgt[j] = weights ? (A)weights[s] : A(1);
   }
   if (VEC) {
     constexpr int N = Vec<T>::N;
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
         Vec<T> o = v;
         if (weights) {
 #pragma unroll
-          for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(Num<T>::to_f(v.v[q]) * wgt[j]);
+          for (int q = 0; q < N; ++q) o.v[q] = Conv<T>::from_acc(Conv<T>::to_acc(v.v[q]) * wgt[j]);
         }
         stv(out + dst[j] + c, o);
       }
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
 #pragma unroll
       for (int j = 0; j < MAXF; ++j) {
         if (j >= F) break;
-        out[dst[j] + c] = weights ? Num<T>::from_f(Num<T>::to_f(v) * wgt[j]) : v;
+        out[dst[j] + c] = weights ? Conv<T>::from_acc(Conv<T>::to_acc(v) * wgt[j]) : v;
       }
     }
   }
@@ -163,6 +168,7 @@ static inline unsigned row_blocks(int64_t rows);
 int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, int h, int dh, const int32_t *order,
                      int64_t n, int dtype, void *out, cudaStream_t st) {
   (void)batch;
+  if (dtype == SMOE_F64) return fail(SMOE_ENOTSUP, "heads_to_grouped: bf16 / fp32 only");
   const int esz = dtype == SMOE_BF16 ? 2 : 4;
   if ((dh * esz) % 16 || (reinterpret_cast<uintptr_t>(heads) | reinterpret_cast<uintptr_t>(out)) % 16)
     return fail(SMOE_ENOTSUP, "heads_to_grouped: d_head * element size must be a multiple of 16 bytes (aligned)");
@@ -178,14 +184,15 @@ int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, i
 // ---- combine ---------------------------------------------------------------
 template <typename T, bool VEC, int JK>
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,
-                                                               const float *__restrict__ p,
+                                                               const typename WOf<T>::type *__restrict__ p,
                                                                int64_t S, int J_, int64_t d,
                                                                T *__restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (s >= S) return;
+  using A = typename AccOf<T>::type;
   const int J = JK > 0 ? JK : J_;   // JK > 0: compile-time k (weights in registers, all k loads in flight)
-  float pw[JK > 0 ? JK : 1];
+  A pw[JK > 0 ? JK : 1];
   if (JK > 0) {
 #pragma unroll
     for (int j = 0; j < (JK > 0 ? JK : 1); ++j) pw[j] = p[s * J + j];
@@ -195,26 +202,26 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
   if (VEC) {
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
-      float acc[N];
+      A acc[N];
 #pragma unroll
-      for (int q = 0; q < N; ++q) acc[q] = 0.f;
+      for (int q = 0; q < N; ++q) acc[q] = 0;
 #pragma unroll
       for (int j = 0; j < (JK > 0 ? JK : J); ++j) {
-        const float pj = JK > 0 ? pw[j] : p[s * J + j];
+        const A pj = JK > 0 ? pw[j] : (A)p[s * J + j];
         Vec<T> v = ldv(src + (int64_t)j * d + c);
 #pragma unroll
-        for (int q = 0; q < N; ++q) acc[q] = fmaf(pj, Num<T>::to_f(v.v[q]), acc[q]);
+        for (int q = 0; q < N; ++q) acc[q] = fma(pj, Conv<T>::to_acc(v.v[q]), acc[q]);
       }
       Vec<T> o;
 #pragma unroll
-      for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(acc[q]);
+      for (int q = 0; q < N; ++q) o.v[q] = Conv<T>::from_acc(acc[q]);
       stv(dst + c, o);
     }
   } else {
     for (int64_t c = lane; c < d; c += 32) {
-      float acc = 0.f;
-      for (int j = 0; j < J; ++j) acc = fmaf(p[s * J + j], Num<T>::to_f(src[(int64_t)j * d + c]), acc);
-      dst[c] = Num<T>::from_f(acc);
+      A acc = 0;
+      for (int j = 0; j < J; ++j) acc = fma((A)p[s * J + j], Conv<T>::to_acc(src[(int64_t)j * d + c]), acc);
+      dst[c] = Conv<T>::from_acc(acc);
     }
   }
 }
@@ -225,27 +232,28 @@ template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRowThreads) combine_grad_p_kernel(const T *__restrict__ dy,
                                                                       const T *__restrict__ y_hat,
                                                                       int64_t S, int J, int64_t d,
-                                                                      float *__restrict__ dp) {
+                                                                      typename WOf<T>::type *__restrict__ dp) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (s >= S) return;
+  using A = typename AccOf<T>::type;
   const T *g = dy + s * d;
   for (int j = 0; j < J; ++j) {
     const T *yh = y_hat + (s * J + j) * d;
-    float acc = 0.f;
+    A acc = 0;
     if (VEC) {
       constexpr int N = Vec<T>::N;
       for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
         Vec<T> a = ldv(g + c), b = ldv(yh + c);
 #pragma unroll
-        for (int q = 0; q < N; ++q) acc = fmaf(Num<T>::to_f(a.v[q]), Num<T>::to_f(b.v[q]), acc);
+        for (int q = 0; q < N; ++q) acc = fma(Conv<T>::to_acc(a.v[q]), Conv<T>::to_acc(b.v[q]), acc);
       }
     } else {
-      for (int64_t c = lane; c < d; c += 32) acc = fmaf(Num<T>::to_f(g[c]), Num<T>::to_f(yh[c]), acc);
+      for (int64_t c = lane; c < d; c += 32) acc = fma(Conv<T>::to_acc(g[c]), Conv<T>::to_acc(yh[c]), acc);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) dp[s * J + j] = acc;
+    if (lane == 0) dp[s * J + j] = (typename WOf<T>::type)acc;
   }
 }
 
@@ -258,31 +266,32 @@ __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__r
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (t >= Trows) return;
+  using A = typename AccOf<T>::type;
   const int F = FK > 0 ? FK : F_;   // FK > 0: compile-time fan-out, all k loads in flight
   const T *src = g + t * F * d;
   T *dst = dx + t * d;
   if (VEC) {
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
-      float acc[N];
+      A acc[N];
 #pragma unroll
-      for (int q = 0; q < N; ++q) acc[q] = 0.f;
+      for (int q = 0; q < N; ++q) acc[q] = 0;
 #pragma unroll
       for (int j = 0; j < (FK > 0 ? FK : F); ++j) {
         Vec<T> v = ldv(src + (int64_t)j * d + c);
 #pragma unroll
-        for (int q = 0; q < N; ++q) acc[q] += Num<T>::to_f(v.v[q]);
+        for (int q = 0; q < N; ++q) acc[q] += Conv<T>::to_acc(v.v[q]);
       }
       Vec<T> o;
 #pragma unroll
-      for (int q = 0; q < N; ++q) o.v[q] = Num<T>::from_f(acc[q]);
+      for (int q = 0; q < N; ++q) o.v[q] = Conv<T>::from_acc(acc[q]);
       stv(dst + c, o);
     }
   } else {
     for (int64_t c = lane; c < d; c += 32) {
-      float acc = 0.f;
-      for (int j = 0; j < F; ++j) acc += Num<T>::to_f(src[(int64_t)j * d + c]);
-      dst[c] = Num<T>::from_f(acc);
+      A acc = 0;
+      for (int j = 0; j < F; ++j) acc += Conv<T>::to_acc(src[(int64_t)j * d + c]);
+      dst[c] = Conv<T>::from_acc(acc);
     }
   }
 }
@@ -293,93 +302,70 @@ __global__ void activation_kernel(const T *__restrict__ x, int64_t numel, int ac
                                   T *__restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float z = Num<T>::to_f(x[i]);
-    out[i] = Num<T>::from_f(deriv ? act_grad(act, z) : act_fwd(act, z));
+    const auto z = Conv<T>::to_acc(x[i]);   // fp32 storage: 64-bit evaluation, one rounding
+    out[i] = Conv<T>::from_acc(deriv ? act_grad(act, z) : act_fwd(act, z));
   }
 }
 
 // ---- dispatch --------------------------------------------------------------
 static inline unsigned row_blocks(int64_t rows) { return (unsigned)((rows + kRowWarps - 1) / kRowWarps); }
 
-int group(const void *x, int64_t d, const int32_t *order, int64_t n, int fan_out,
-          const float *w, int dtype, void *out, cudaStream_t st) {
+int group(const void *x, int64_t d, const int32_t *order, int64_t n, int fan_out, const void *w, int dtype,
+          void *out, cudaStream_t st) {
   if (n == 0 || d == 0) return SMOE_OK;
-  if (dtype == SMOE_BF16) {
-    using T = __nv_bfloat16;
-    if (vec_ok(x, d, 2) && vec_ok(out, d, 2))
-      group_kernel<T, true><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
+  SMOE_DTYPE_DISPATCH(dtype, {
+    using W = typename WOf<T>::type;
+    if (vec_ok(x, d, sizeof(T)) && vec_ok(out, d, sizeof(T)))
+      group_kernel<T, true><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out,
+                                                                   (const W *)w, (T *)out);
     else
-      group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
-  } else {
-    using T = float;
-    if (vec_ok(x, d, 4) && vec_ok(out, d, 4))
-      group_kernel<T, true><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
-    else
-      group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out, w, (T *)out);
-  }
+      group_kernel<T, false><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, fan_out,
+                                                                    (const W *)w, (T *)out);
+  });
   return check_launch("group");
 }
 
-int group_inv(const void *x, int64_t t_rows, int64_t d, const int32_t *inv, int fan_out, const float *w, int dtype,
+int group_inv(const void *x, int64_t t_rows, int64_t d, const int32_t *inv, int fan_out, const void *w, int dtype,
               void *out, cudaStream_t st) {
   if (t_rows == 0 || d == 0) return SMOE_OK;
-  if (dtype == SMOE_BF16) {
-    using T = __nv_bfloat16;
-    if (vec_ok(x, d, 2) && vec_ok(out, d, 2))
+  SMOE_DTYPE_DISPATCH(dtype, {
+    using W = typename WOf<T>::type;
+    if (vec_ok(x, d, sizeof(T)) && vec_ok(out, d, sizeof(T)))
       SMOE_FANOUT_DISPATCH(fan_out, (group_inv_kernel<T, true, FKC><<<row_blocks(t_rows), kRowThreads, 0, st>>>(
-                                        (const T *)x, d, inv, t_rows, fan_out, w, (T *)out)));
+                                        (const T *)x, d, inv, t_rows, fan_out, (const W *)w, (T *)out)));
     else
       group_inv_kernel<T, false, 0><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
-                                                                                 w, (T *)out);
-  } else {
-    using T = float;
-    if (vec_ok(x, d, 4) && vec_ok(out, d, 4))
-      SMOE_FANOUT_DISPATCH(fan_out, (group_inv_kernel<T, true, FKC><<<row_blocks(t_rows), kRowThreads, 0, st>>>(
-                                        (const T *)x, d, inv, t_rows, fan_out, w, (T *)out)));
-    else
-      group_inv_kernel<T, false, 0><<<row_blocks(t_rows), kRowThreads, 0, st>>>((const T *)x, d, inv, t_rows, fan_out,
-                                                                                 w, (T *)out);
-  }
+                                                                                 (const W *)w, (T *)out);
+  });
   return check_launch("group_inv");
 }
 
-int combine(const void *y_hat, const float *p, int64_t S, int J, int64_t d, int dtype, void *y,
-            cudaStream_t st) {
+int combine(const void *y_hat, const void *p, int64_t S, int J, int64_t d, int dtype, void *y, cudaStream_t st) {
   if (S == 0 || d == 0) return SMOE_OK;
-  if (dtype == SMOE_BF16) {
-    using T = __nv_bfloat16;
-    if (vec_ok(y_hat, d, 2) && vec_ok(y, d, 2))
+  SMOE_DTYPE_DISPATCH(dtype, {
+    using W = typename WOf<T>::type;
+    if (vec_ok(y_hat, d, sizeof(T)) && vec_ok(y, d, sizeof(T)))
       SMOE_FANOUT_DISPATCH(J, (combine_kernel<T, true, FKC><<<row_blocks(S), kRowThreads, 0, st>>>(
-                                  (const T *)y_hat, p, S, J, d, (T *)y)));
+                                  (const T *)y_hat, (const W *)p, S, J, d, (T *)y)));
     else
-      combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
-  } else {
-    using T = float;
-    if (vec_ok(y_hat, d, 4) && vec_ok(y, d, 4))
-      SMOE_FANOUT_DISPATCH(J, (combine_kernel<T, true, FKC><<<row_blocks(S), kRowThreads, 0, st>>>(
-                                  (const T *)y_hat, p, S, J, d, (T *)y)));
-    else
-      combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, p, S, J, d, (T *)y);
-  }
+      combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, (const W *)p, S, J, d,
+                                                                         (T *)y);
+  });
   return check_launch("combine");
 }
 
-int combine_grad_p(const void *dy, const void *y_hat, int64_t S, int J, int64_t d, int dtype,
-                   float *dp, cudaStream_t st) {
+int combine_grad_p(const void *dy, const void *y_hat, int64_t S, int J, int64_t d, int dtype, void *dp,
+                   cudaStream_t st) {
   if (S == 0) return SMOE_OK;
-  if (dtype == SMOE_BF16) {
-    using T = __nv_bfloat16;
-    if (vec_ok(dy, d, 2) && vec_ok(y_hat, d, 2))
-      combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
+  SMOE_DTYPE_DISPATCH(dtype, {
+    using W = typename WOf<T>::type;
+    if (vec_ok(dy, d, sizeof(T)) && vec_ok(y_hat, d, sizeof(T)))
+      combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d,
+                                                                            (W *)dp);
     else
-      combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
-  } else {
-    using T = float;
-    if (vec_ok(dy, d, 4) && vec_ok(y_hat, d, 4))
-      combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
-    else
-      combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d, dp);
-  }
+      combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d,
+                                                                             (W *)dp);
+  });
   return check_launch("combine_grad_p");
 }
 
@@ -401,36 +387,23 @@ int dp_from_partials(const float *part, int64_t n, int parts, const int32_t *ord
   return check_launch("dp_from_partials");
 }
 
-int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx,
-                  cudaStream_t st) {
+int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx, cudaStream_t st) {
   if (Trows == 0 || d == 0) return SMOE_OK;
-  if (dtype == SMOE_BF16) {
-    using T = __nv_bfloat16;
-    if (vec_ok(g, d, 2) && vec_ok(dx, d, 2))
+  SMOE_DTYPE_DISPATCH(dtype, {
+    if (vec_ok(g, d, sizeof(T)) && vec_ok(dx, d, sizeof(T)))
       SMOE_FANOUT_DISPATCH(F, (fanout_reduce_kernel<T, true, FKC><<<row_blocks(Trows), kRowThreads, 0, st>>>(
                                   (const T *)g, Trows, F, d, (T *)dx)));
     else
       fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
-  } else {
-    using T = float;
-    if (vec_ok(g, d, 4) && vec_ok(dx, d, 4))
-      SMOE_FANOUT_DISPATCH(F, (fanout_reduce_kernel<T, true, FKC><<<row_blocks(Trows), kRowThreads, 0, st>>>(
-                                  (const T *)g, Trows, F, d, (T *)dx)));
-    else
-      fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
-  }
+  });
   return check_launch("fanout_reduce");
 }
 
-int activation(const void *x, int64_t numel, int act, int deriv, int dtype, void *out,
-               cudaStream_t st) {
+int activation(const void *x, int64_t numel, int act, int deriv, int dtype, void *out, cudaStream_t st) {
   if (numel == 0) return SMOE_OK;
   int64_t blocks64 = (numel + 255) / 256;
   unsigned blocks = (unsigned)(blocks64 < 148 * 32 ? blocks64 : 148 * 32);
-  if (dtype == SMOE_BF16)
-    activation_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16 *)x, numel, act, deriv, (__nv_bfloat16 *)out);
-  else
-    activation_kernel<float><<<blocks, 256, 0, st>>>((const float *)x, numel, act, deriv, (float *)out);
+  SMOE_DTYPE_DISPATCH(dtype, (activation_kernel<T><<<blocks, 256, 0, st>>>((const T *)x, numel, act, deriv, (T *)out)));
   return check_launch("activation");
 }
 

@@ -5,10 +5,13 @@ scatter2scatter (:143-220), scatter_combine (:242-286), group (:289-326),
 group_xty (:329-361), LayoutFlag + the four layout constants (:61-72),
 TileConfig (:46-58), the MAC counter (:74-98) and the fault hook (:100-107).
 
-Arguments are torch CUDA tensors: activations (rows, cols) in bfloat16 or
-float32, expert stacks (E, d_in, d_out) of the same dtype, combine weights in
-float32.  Every call enqueues sm_100a kernels from libsmoe_b200.so on the
-current stream; nothing here computes on the CPU and there is no fallback.
+Arguments are torch CUDA tensors: activations (rows, cols) in bfloat16 (the
+tcgen05 product path), float32 (the check mode: 64-bit accumulation, one
+rounding) or float64 (the reference's verification dtype), expert stacks
+(E, d_in, d_out) of the same dtype, combine weights in float32 (float64 with
+float64 storage).  Every call enqueues sm_100a kernels from libsmoe_b200.so on
+the current stream; nothing here computes on the CPU and there is no fallback:
+a bf16 call the tensor-core engine cannot take raises NotImplementedError.
 
 TileConfig is accepted for API compatibility and ignored: the GPU kernels
 choose their own tiles, and results never depend on tiling (the reference's
@@ -126,7 +129,14 @@ def _dtype_id(t: torch.Tensor) -> int:
         return _lib.SMOE_BF16
     if t.dtype == torch.float32:
         return _lib.SMOE_F32
-    raise ValueError(f"unsupported element type {t.dtype}; use bfloat16 or float32")
+    if t.dtype == torch.float64:
+        return _lib.SMOE_F64
+    raise ValueError(f"unsupported element type {t.dtype}; use bfloat16, float32 or float64")
+
+
+def _wdtype(t: torch.Tensor) -> torch.dtype:
+    """Element type of per-slot weights / dp for storage like t (include/smoe_b200.h smoe_dtype)."""
+    return torch.float64 if t.dtype == torch.float64 else torch.float32
 
 
 def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
@@ -275,7 +285,7 @@ def scatter_combine(
         raise ValueError(
             f"scattered input rows ({x.shape[0]}) * fan_out ({fan_out}) must equal T*k ({num_slots})")
     x, w = _cuda(x, "x"), _cuda(w, "w")
-    p32 = _cuda(p_flat.to(torch.float32), "p_flat")
+    p32 = _cuda(p_flat.to(_wdtype(x)), "p_flat")
     rows = num_slots // combine_cols
     if (x.dtype == torch.bfloat16 and combine_cols > 2 and _COMBINE_FUSED != "1"
             and (engine or _engine) != "simt") or _COMBINE_FUSED == "0":
@@ -286,8 +296,8 @@ def scatter_combine(
         # memory the fused form saves.
         y_hat = scatter2scatter(x, w, order, fan_out, LayoutFlag(grouped_in, False), engine=engine)
         return combine(p32.view(rows, combine_cols), y_hat)
-    acc = torch.empty((rows, d_out), dtype=torch.float32, device=x.device)
-    y = acc if x.dtype == torch.float32 else torch.empty((rows, d_out), dtype=x.dtype, device=x.device)
+    acc = torch.empty((rows, d_out), dtype=_wdtype(x), device=x.device)
+    y = acc if x.dtype != torch.bfloat16 else torch.empty((rows, d_out), dtype=x.dtype, device=x.device)
     t0 = _lt.begin()
     st = _lib.load().smoe_scatter_combine(
         x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], d_in, d_out, order.o.data_ptr(),
@@ -312,10 +322,10 @@ def group(
     num_slots = order.num_slots
     if x.shape[0] * fan_out != num_slots:
         raise ValueError(f"input rows ({x.shape[0]}) * fan_out ({fan_out}) must equal T*k ({num_slots})")
+    x = _cuda(x, "x")
     if weights is not None:
         require_dims(tuple(weights.shape) == (num_slots,), "slot weights", tuple(weights.shape), (num_slots,))
-        weights = _cuda(weights.to(torch.float32), "weights")
-    x = _cuda(x, "x")
+        weights = _cuda(weights.to(_wdtype(x)), "weights")
     if out is None:
         out = torch.empty((num_slots, x.shape[1]), dtype=x.dtype, device=x.device)
     else:
@@ -518,7 +528,7 @@ def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = Non
     """Y[s] = sum_i p[s, i] * Y_hat[s*j + i]  (parallel_linear.py:69-73)."""
     s, j = p.shape
     y_hat = _cuda(y_hat, "y_hat")
-    p32 = _cuda(p.to(torch.float32), "p")
+    p32 = _cuda(p.to(_wdtype(y_hat)), "p")
     if out is None:
         out = torch.empty((s, y_hat.shape[1]), dtype=y_hat.dtype, device=y_hat.device)
     t0 = _lt.begin()
@@ -532,7 +542,7 @@ def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = Non
 def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int) -> torch.Tensor:
     """dp[s, i] = <dY[s], Y_hat[s*j + i]>  (parallel_linear.py:198-206), float32."""
     dy, y_hat = _cuda(dy, "dy"), _cuda(y_hat, "y_hat")
-    dp = torch.empty((s, j), dtype=torch.float32, device=dy.device)
+    dp = torch.empty((s, j), dtype=_wdtype(dy), device=dy.device)
     t0 = _lt.begin()
     st = _lib.load().smoe_combine_grad_p(dy.data_ptr(), y_hat.data_ptr(), s, j, dy.shape[1],
                                          _dtype_id(dy), dp.data_ptr(), _stream(dy))

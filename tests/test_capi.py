@@ -21,7 +21,7 @@ def declared_functions():
 def test_library_exists_and_loads():
     assert _lib.LIB_PATH.exists(), "run python -m paper_2403_08245_b200.build"
     lib = _lib.load()
-    assert lib.smoe_abi_version() == 2
+    assert lib.smoe_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_every_declared_symbol_is_exported_and_bound():
@@ -90,3 +90,18 @@ def test_sm100a_code_in_library():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([cuobjdump, "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_bf16_never_falls_back_to_simt():
+    """A bf16 GEMM the tcgen05 engine cannot take is refused (SMOE_ENOTSUP), never
+    silently re-routed to the SIMT kernels.  Without a GPU the
+    refusal is "no sm_100a device"; on the B200 it names the unsupported shape
+    (tests/test_kernels_gpu.py::test_bf16_unsupported_shape_is_refused)."""
+    lib = _lib.load()
+    # d_out = 12 (not a multiple of 8), scattered in/out, bf16, engine AUTO; buffers are fake
+    fake = 1 << 20
+    st = lib.smoe_scatter2scatter(fake, 4, fake, 2, 16, 12, fake, fake, 8, 2, 0, 0, 0, _lib.SMOE_BF16, 0, 0,
+                                  fake, None, None, _lib.ENGINE_IDS["auto"], None)
+    assert st == _lib.SMOE_ENOTSUP, _lib.last_error()
+    st = lib.smoe_group_xty(fake, fake, fake, 2, 8, 16, 12, _lib.SMOE_BF16, fake, _lib.ENGINE_IDS["auto"], None)
+    assert st == _lib.SMOE_ENOTSUP, _lib.last_error()

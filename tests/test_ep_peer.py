@@ -56,31 +56,34 @@ def test_dispatch_layout_matches_local_grouped_order(world, e):
         assert off_me.tolist() == off.tolist()
 
 
-T_LOCAL, D, DE = 512, 256, 512
-SHAPES = {"c1": (8, 2), "c4": (64, 8), "starve": (8, 2)}  # (E, k); "starve": every token routed to rank 0's experts
+# (E, k, T_local, d_model, d_expert); "starve": every token routed to rank 0's experts;
+# "c4full": BASELINE configs[4] per rank (E=64, k=8, d_model=4096, d_expert=1792, T_local=32768)
+SHAPES = {"c1": (8, 2, 512, 256, 512), "c4": (64, 8, 512, 256, 512), "starve": (8, 2, 512, 256, 512),
+          "c4full": (64, 8, 32768, 4096, 1792)}
 
 
-def _problem(world, E):
-    g = torch.Generator().manual_seed(11)
-    x = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
-    dy = (torch.rand(world * T_LOCAL, D, generator=g) * 2 - 1).bfloat16()
-    w1 = ((torch.rand(E, D, DE, generator=g) * 2 - 1) / D ** 0.5).bfloat16()
-    w2 = ((torch.rand(E, DE, D, generator=g) * 2 - 1) / DE ** 0.5).bfloat16()
-    logits = torch.randn(world * T_LOCAL, E, generator=g)
+def _problem(world, shape):
+    E, _, t_local, D, DE = SHAPES[shape]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.rand(world * t_local, D, generator=g, device="cuda") * 2 - 1).bfloat16()
+    dy = (torch.rand(world * t_local, D, generator=g, device="cuda") * 2 - 1).bfloat16()
+    w1 = ((torch.rand(E, D, DE, generator=g, device="cuda") * 2 - 1) / D ** 0.5).bfloat16()
+    w2 = ((torch.rand(E, DE, D, generator=g, device="cuda") * 2 - 1) / DE ** 0.5).bfloat16()
+    logits = torch.randn(world * t_local, E, generator=g, device="cuda")
     logits[:40, 0] += 8.0        # skew: many rows to expert 0 (owned by rank 0)
     return x, dy, w1, w2, logits
 
 
 def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
     os.environ["SMOE_EP_FUSED_RETURN"] = fused
-    E, K = SHAPES[shape]
+    E, K, T_LOCAL = SHAPES[shape][:3]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2403_08245_b200 as sm
         from paper_2403_08245_b200.ep_peer import PeerExpertParallelSmoeMlp
         torch.cuda.set_device(0)
-        x, dy, w1, w2, logits = (a.cuda() for a in _problem(world, E))
+        x, dy, w1, w2, logits = _problem(world, shape)
         if shape == "starve":            # the other ranks' experts receive no rows at all
             logits[:, : E // world] += 100.0
         routing = sm.topk_select(torch.softmax(logits, 1), K)
@@ -118,7 +121,8 @@ def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,fused,shape,scaled", [
     (2, "1", "c1", False), (4, "1", "c1", False), (2, "0", "c1", False), (4, "1", "c4", False),
-    (2, "1", "starve", False), (2, "1", "c1", True), (4, "1", "c4", True), (2, "1", "starve", True)])
+    (2, "1", "starve", False), (2, "1", "c1", True), (4, "1", "c4", True), (2, "1", "starve", True),
+    (2, "1", "c4full", True)])
 def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape, scaled):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     ctx = mp.get_context("spawn")

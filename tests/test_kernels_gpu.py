@@ -284,3 +284,33 @@ def test_group_token_major_equals_grouped_walk(k, weighted, dtype):
     finally:
         sm.kernels._GROUP_BY_TOKEN = prev
     assert torch.equal(got, want)
+
+
+def test_bf16_unsupported_shape_is_refused():
+    """bf16 with d_out % 8 != 0: NotImplementedError (SMOE_ENOTSUP), no SIMT fallback;
+    the same call with engine='simt' (explicit cross-check) still runs."""
+    rng = np.random.default_rng(5)
+    idx = np.stack([rng.permutation(4)[:2] for _ in range(16)]).astype(np.int64)
+    order = order_of(idx, 4)
+    x = t(rng.standard_normal((16, 16)).astype(np.float32), torch.bfloat16)
+    w = t(rng.standard_normal((4, 16, 12)).astype(np.float32), torch.bfloat16)
+    with pytest.raises(NotImplementedError, match="no SIMT fallback"):
+        sm.scatter2scatter(x, w, order, 2, sm.SCATTERED_TO_GROUPED)
+    y = sm.scatter2scatter(x, w, order, 2, sm.SCATTERED_TO_GROUPED, engine="simt")
+    o_ref, off_ref = orc.compute_grouped_order(idx, 4)
+    want = orc.scatter2scatter(np_of(x), np_of(w), o_ref, off_ref, 2, False, True)
+    assert rel_err(y, want) < 2e-2
+
+
+def test_fp32_check_mode_accumulates_in_64_bit():
+    """The check mode rounds once from a 64-bit sum (core_tensor.py:1-7): the
+    reference's known case [2^24, 1, -2^24] . 1 = 1 (test_core_tensor.py:32-37),
+    which fp32 accumulation gets wrong (0)."""
+    order = order_of(np.zeros((1, 1), dtype=np.int64), 1)
+    x = t(np.array([[2.0 ** 24, 1.0, -(2.0 ** 24)]], dtype=np.float32))
+    w = t(np.ones((1, 3, 1), dtype=np.float32))
+    y = sm.scatter2scatter(x, w, order, 1, sm.SCATTERED_TO_SCATTERED)
+    assert float(y[0, 0]) == 1.0
+    dw = sm.group_xty(t(np.array([[2.0 ** 24], [1.0], [-(2.0 ** 24)]], dtype=np.float32)),
+                      t(np.ones((3, 1), dtype=np.float32)), order_of(np.zeros((3, 1), dtype=np.int64), 1))
+    assert float(dw[0, 0, 0]) == 1.0

@@ -73,3 +73,48 @@ def test_heads_to_grouped_matches_permute_and_group(dtype):
     want = slots[order.o.long()]
     got = sm.kernels.heads_to_grouped(heads, order, k)
     assert torch.equal(got, want)
+
+
+def test_momha_c3_full_size_vs_oracle():
+    """C3 (E=16, k=4, d_model=2048, d_head=128, seq 4096, B=8 -> T=32768) in bf16 vs the oracle.
+
+    dY is zero outside one sampled sequence b.  Attention never crosses a
+    sequence, so every gradient then equals the oracle's gradients of that
+    sequence alone (oracle/scattermlp_oracle.py momha_forward/backward,
+    moe_layers.py:406-482): Y, dX and dp rows of sequence b, and the FULL weight
+    gradients dWq, dWk, dWv, dWo — produced by the routed projection GEMMs at
+    full C3 size (bins over all 32768 tokens, zero rows included).
+    """
+    from gpu_util import bf16_round
+    from oracle import scattermlp_oracle as orc
+
+    cfg = sm.MomhaConfig(d_model=2048, d_head=128, num_heads=16, heads_per_expert=4, num_experts=16, k=4)
+    seq, b = 4096, 8
+    rng = np.random.default_rng(7)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = (torch.rand((b * seq, 2048), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    wts = sm.init_momha_weights(cfg, 5, dtype=torch.bfloat16)
+    logits = torch.randn((b * seq, 16), device="cuda", generator=g)
+    routing = sm.topk_select(torch.softmax(logits, 1), 4)
+    order = sm.compute_grouped_order(routing)
+    sb = int(rng.integers(b))
+    lo, hi = sb * seq, (sb + 1) * seq
+    dy = torch.zeros((b * seq, 2048), device="cuda", dtype=torch.bfloat16)
+    dy[lo:hi] = (torch.rand((seq, 2048), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    y, ctx = sm.momha_forward(x, wts, routing, order, cfg, seq)
+    gr = sm.momha_backward(ctx, dy)
+    torch.cuda.synchronize()
+
+    xs = np_of(x[lo:hi])
+    idx = routing.expert_idx[lo:hi].cpu().numpy()
+    p = routing.p[lo:hi].cpu().numpy()
+    wq, wk, wv, wo = (np_of(getattr(wts, f)) for f in ("wq", "wk", "wv", "wo"))
+    want_y, st = orc.momha_forward(xs, wq, wk, wv, wo, idx, p, 16, seq, 128)
+    want = orc.momha_backward(xs, wq, wk, wv, wo, p, st, np_of(dy[lo:hi]))
+    assert rel_err(y[lo:hi], want_y) <= 2e-2
+    errs = {"dx": rel_err(gr.dx[lo:hi], want[0]), "dp": rel_err(gr.dp[lo:hi], want[5]),
+            "dwq": rel_err(gr.dwq, want[1]), "dwk": rel_err(gr.dwk, want[2]),
+            "dwv": rel_err(gr.dwv, want[3]), "dwo": rel_err(gr.dwo, want[4])}
+    assert all(v <= 2e-2 for v in errs.values()), errs
+    # tokens outside the sampled sequence get no gradient
+    assert float(gr.dx[:lo].abs().max() if lo else 0.0) == 0.0

@@ -99,6 +99,17 @@ def test_smoe_mlp_forward_backward():
             np.testing.assert_allclose(got, g[pre + name], rtol=RTOL, atol=1e-6, err_msg=f"{j}:{name}")
 
 
+def test_momha_forward_backward():
+    """The attention-layer restatement (moe_layers.py:270-482) against the reference's outputs."""
+    g = load_golden("momha")
+    seq_len, d_head = int(g["seq_len"]), 4
+    y, st = orc.momha_forward(g["x"], g["wq"], g["wk"], g["wv"], g["wo"], g["idx"], g["p"], 3, seq_len, d_head)
+    np.testing.assert_allclose(y, g["y"], rtol=RTOL, atol=ATOL)
+    got = orc.momha_backward(g["x"], g["wq"], g["wk"], g["wv"], g["wo"], g["p"], st, g["dy"])
+    for val, name in zip(got, ("dx", "dwq", "dwk", "dwv", "dwo", "dp")):
+        np.testing.assert_allclose(val, g[name], rtol=RTOL, atol=1e-6, err_msg=name)
+
+
 @pytest.mark.parametrize("name", ["gelu", "relu", "silu"])
 def test_activations(name):
     g = load_golden("mlp")
