@@ -81,9 +81,20 @@ def _measure_in_process(config: str, tokens: int, warmup: int, repeats: int, see
         y, ctx = scattermlp.smoe_mlp_forward(x, w1, w2, routing, order, training=True)
         scattermlp.smoe_mlp_backward(ctx, dy)
 
-    med, p5, p95 = bench.time_callable(step, warmup, repeats)
+    # the reference's own protocol (bench.time_callable, bench.py:86-100) plus the mean
+    samples = []
+
+    def timed():
+        t0 = time.perf_counter_ns()
+        step()
+        samples.append(time.perf_counter_ns() - t0)
+
+    med, p5, p95 = bench.time_callable(timed, warmup, repeats)
+    samples = samples[max(warmup, 0):]
+    mean_s = sum(samples) / len(samples) * 1e-9
     return {"config": config, "tokens": tokens, "median_s": med * 1e-9, "p5_s": p5 * 1e-9, "p95_s": p95 * 1e-9,
-            "tokens_per_s": tokens / (med * 1e-9), "repeats": repeats, "warmup": warmup,
+            "mean_s": mean_s, "tokens_per_s": tokens / (med * 1e-9), "tokens_per_s_mean": tokens / mean_s,
+            "repeats": repeats, "warmup": warmup,
             "problem_build_s": t_build, "flops_per_step": 12.0 * tokens * k * d * de,
             "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
             "scattermlp_workers": os.environ.get("SCATTERMLP_WORKERS")}

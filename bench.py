@@ -21,9 +21,11 @@ roofline: the dominant kernel (the GEMM with the largest share of the step,
          `roofline_gather` reports the layer-1 gather GEMM the same way.
          `kernels` lists every library call's per-launch time and share of
          the step from the same events.
-cpu_baseline: the CPU oracle (NumPy restatement of the reference, oracle/)
-         on a bounded sample (T=128 at C1 dims), rank 0 at N=1 only.
---impl reference: the same metric from the oracle port on the host CPU.
+cpu_baseline: the unmodified reference (scattermlp, vendored to baseline/_ref)
+         on the host cores, one fwd+bwd of a bounded sample (T=256 tokens at
+         C1 dims), rank 0 at N=1 only (baseline/cpu_reference.py).
+--impl reference: the same metric from the unmodified reference on the host
+         CPU, --steps steps of T=256 tokens after --warmup untimed ones.
 """
 from __future__ import annotations
 
@@ -129,10 +131,18 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU legs (oracle port): cpu_baseline and --impl reference
+# CPU legs: cpu_baseline and --impl reference
+#
+# Both time the UNMODIFIED reference (scattermlp, installed into baseline/_ref
+# by baseline/vendor_reference.py) through its own public API on the host
+# cores (baseline/cpu_reference.py: SCATTERMLP_WORKERS = all cores, one BLAS
+# thread each — the faster of the reference's two thread configurations at
+# C1 dims).  Only if baseline/_ref is absent do they fall back to the oracle
+# port (oracle/scattermlp_oracle.py) and say so ("kind": "port").
+
 
 def cpu_oracle_step_time(T, d, de, E, k, seed=0):
-    """One fwd+bwd of the oracle port on T tokens; returns seconds (after one warm call at tiny T)."""
+    """One fwd+bwd of the oracle port on T tokens; returns seconds."""
     import numpy as np
     from oracle import scattermlp_oracle as orc
 
@@ -153,29 +163,48 @@ def cpu_oracle_step_time(T, d, de, E, k, seed=0):
     return time.perf_counter() - t0
 
 
+def cpu_reference(config, tokens, warmup, repeats):
+    """dict(value tok/s, ms_per_step, p5/p95, cores, kind, sample) for the CPU reference."""
+    from baseline import cpu_reference as cref
+
+    if cref.available():
+        r = cref.measure(config, tokens, threads="workers", warmup=warmup, repeats=repeats)
+        return {"value": r["tokens_per_s_mean"], "ms_per_step": 1e3 * r["mean_s"],
+                "ms_median": 1e3 * r["median_s"], "ms_p5": 1e3 * r["p5_s"], "ms_p95": 1e3 * r["p95_s"],
+                "cores": r["cores"], "kind": "reference", "cpu_model": r["cpu_model"],
+                "sample": f"T={tokens} tokens at {config} dims per step, {repeats} step(s): the unmodified reference "
+                          f"(scattermlp from baseline/_ref, smoe_mlp_forward + smoe_mlp_backward, f32 storage / "
+                          f"f64 accumulate), SCATTERMLP_WORKERS={r['cores']}, one BLAS thread per worker"}
+    T, d, de, E, k, _ = CONFIGS[config]
+    for _ in range(warmup):
+        cpu_oracle_step_time(tokens, d, de, E, k)
+    times = [cpu_oracle_step_time(tokens, d, de, E, k) for _ in range(max(repeats, 1))]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    times.sort()
+    return {"value": tokens * len(times) / sum(times), "ms_per_step": 1e3 * sum(times) / len(times),
+            "ms_median": 1e3 * times[len(times) // 2], "ms_p5": 1e3 * times[0], "ms_p95": 1e3 * times[-1],
+            "cores": cores, "kind": "port",
+            "sample": f"T={tokens} tokens at {config} dims per step (oracle/scattermlp_oracle.py port; "
+                      f"baseline/_ref absent)"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference's path on the host CPU."""
+    """--impl reference: the reference's own CPU implementation of the path on the host cores."""
     if rank != 0:
         return
     T, d, de, E, k, desc = CONFIGS[args.config]
-    sample_t = args.ref_tokens
-    for _ in range(args.warmup):
-        cpu_oracle_step_time(sample_t, d, de, E, k)
-    times = [cpu_oracle_step_time(sample_t, d, de, E, k) for _ in range(args.steps)]
-    total = sum(times)
-    tok_s = sample_t * len(times) / total
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    r = cpu_reference(args.config, args.ref_tokens, args.warmup, args.steps)
     line = {
-        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "ms_per_step_median": r["ms_median"], "ms_per_step_p5": r["ms_p5"], "ms_per_step_p95": r["ms_p95"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 storage, f64 accumulate",
-        "data": "synthetic",
-        "config": {"workload": desc, "sample_tokens_per_step": sample_t},
-        "tflops": flops_per_step(sample_t, d, de, E, k) * len(times) / total / 1e12,
-        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"T={sample_t} tokens at {args.config} dims per step (oracle/scattermlp_oracle.py, "
-                                   f"NumPy/OpenBLAS f64 accumulate)"},
-        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic (the reference's own bench._mlp_problem draws)",
+        "config": {"workload": desc, "sample_tokens_per_step": args.ref_tokens},
+        "tflops": flops_per_step(args.ref_tokens, d, de, E, k) / (r["ms_per_step"] / 1e3) / 1e12,
+        "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"], "cpu_model": r.get("cpu_model")},
+        "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -267,13 +296,25 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event per step boundary gives the per-step distribution (median / p5 / p95)
+    ev_steps = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     from paper_2403_08245_b200.launch_timer import LaunchTimer
+    mem_before = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
     with LaunchTimer() as lt:   # per-call CUDA events on the launching stream, inside the timed region
         e0.record(st)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             step(x, dy, routing)
+            ev_steps[i].record(st)
         e1.record(st)
     torch.cuda.synchronize()
+    # memory of the timed steps alone (before the e2e / roofline sections allocate more)
+    peak_step_bytes = torch.cuda.max_memory_allocated(dev)
+    step_ms = sorted([e0.elapsed_time(ev_steps[0])] +
+                     [ev_steps[i - 1].elapsed_time(ev_steps[i]) for i in range(1, args.steps)])
+
+    def pct(q):
+        return step_ms[min(len(step_ms) - 1, int(round(q * (len(step_ms) - 1))))]
     t_win1 = sampler.mark()
     barrier()
     clocks = sampler.stop((t_win0, t_win1))
@@ -430,12 +471,9 @@ def run_ours(args, rank, world, local_rank):
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample_t = args.ref_tokens
-        secs = cpu_oracle_step_time(sample_t, d, de, E, k)
-        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        cpu_baseline = {"value": sample_t / secs, "unit": "tokens/s", "cores": cores, "kind": "port",
-                        "sample": f"one fwd+bwd of T={sample_t} tokens at {args.config} dims "
-                                  f"(oracle/scattermlp_oracle.py, NumPy/OpenBLAS, f64 accumulate), {secs:.1f} s"}
+        r = cpu_reference(args.config, args.ref_tokens, 0, 1)
+        cpu_baseline = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": r["kind"],
+                        "sample": r["sample"] + f"; {r['ms_per_step'] / 1e3:.1f} s", "cpu_model": r.get("cpu_model")}
 
     if rank == 0:
         line = {
@@ -467,7 +505,13 @@ def run_ours(args, rank, world, local_rank):
             "kernels": kernels,
             "cpu_baseline": cpu_baseline,
             "clocks": clocks,
-            "peak_memory_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+            "step_ms": {"median": pct(0.5), "p5": pct(0.05), "p95": pct(0.95), "mean": ms,
+                        "n": len(step_ms), "timing": "CUDA events at every step boundary on the launching stream"},
+            # peak over the timed steps only: inputs + weights + the step's working set;
+            # the e2e buffers and the roofline section allocate after this is read
+            "peak_memory_gb": peak_step_bytes / 1e9,
+            "memory": {"resident_before_steps_gb": mem_before / 1e9, "peak_during_steps_gb": peak_step_bytes / 1e9,
+                       "step_working_set_gb": (peak_step_bytes - mem_before) / 1e9},
         }
         print(json.dumps(line), flush=True)
 
@@ -475,17 +519,25 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 100 on the GPU; 3 for --impl reference, ~10 s each)")
+    ap.add_argument("--warmup", type=int, default=None,
+                    help="untimed warm-up steps (default 10 on the GPU; 1 for --impl reference)")
     ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-tokens", type=int, default=128)
+    ap.add_argument("--ref-tokens", type=int, default=256,
+                    help="tokens per CPU reference step (a bounded sample of the workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default=None)
     ap.add_argument("--ep", default="auto", choices=["auto", "peer", "nccl", "none"],
                     help="expert-parallel exchange (auto: peer memory when N>1, none at N=1; "
                          "peer/nccl at N=1 time the EP path on one GPU)")
     args = ap.parse_args()
+    cpu_arm = args.impl == "reference"
+    if args.steps is None:
+        args.steps = 3 if cpu_arm else 100
+    if args.warmup is None:
+        args.warmup = 1 if cpu_arm else 10
     args.warmup = max(args.warmup, 0)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
