@@ -240,7 +240,7 @@ def run_ours(args, rank, world, local_rank):
     cfg = sm.SmoeMlpConfig(d_model=d, d_expert=de, num_experts=e_local, k=min(k, e_local))
     w1, w2 = sm.init_smoe_mlp_weights(cfg, 101 + rank, dtype=dtype, device=dev, source="device")
     wg = (torch.rand((d, E), generator=g, device=dev) * 2 - 1) / (d ** 0.5)
-    routing = sm.topk_select(sm.gate_forward(x.float(), wg), k)
+    routing = sm.gate_topk(x, wg, k)   # gate GEMM + softmax + top-k in one kernel (router.cu)
     torch.cuda.synchronize()
 
     ep_mode = args.ep if args.ep != "auto" else ("peer" if world > 1 else "none")

@@ -113,6 +113,16 @@ int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
  */
 int smoe_router_topk(const float *in, int64_t T, int32_t num_experts, int32_t k, int32_t apply_softmax,
                      int32_t renormalize, float *gate_out, int64_t *expert_idx, float *p, void *stream);
+/* Gate GEMM fused into the router (router.py:119-151):
+ * logits = x @ w_gate accumulated in float64 (never rounded), softmax in float64
+ * rounded once to float32 (gate_out [T, E], may be NULL), stable top-k on the
+ * float32 gates (ties -> lower id) into expert_idx [T, k] int64, p [T, k]
+ * renormalised in float64 when `renormalize`.  x [T, d_model] bf16 or fp32
+ * (x_dtype); w_gate [d_model, E] fp32; k <= 8.
+ * The ids feed smoe_route_sort directly. */
+int smoe_router_gate(const void *x, int32_t x_dtype, const float *w_gate, int64_t T, int32_t d_model,
+                     int32_t num_experts, int32_t k, int32_t renormalize, float *gate_out, int64_t *expert_idx,
+                     float *p, void *stream);
 int smoe_router_backward(const float *gate, const int64_t *expert_idx, const float *grad_p, int64_t T,
                          int32_t num_experts, int32_t k, int32_t renormalized, float *dlogits, void *stream);
 

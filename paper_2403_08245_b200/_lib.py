@@ -37,6 +37,7 @@ SIGNATURES = {
     "smoe_route_sort": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "smoe_router_topk": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smoe_router_backward": (_c.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_router_gate": (_c.c_int, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smoe_scatter2scatter": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
                                         _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
     "smoe_group_xty": (_c.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _i32, _vp]),

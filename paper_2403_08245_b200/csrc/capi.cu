@@ -45,6 +45,8 @@ int simt_scatter_combine(const void *, const void *, int, int64_t, int64_t, cons
                          const void *, int, int, int, void *, void *, cudaStream_t);
 int router_topk(const float *, int64_t, int, int, int, int, float *, int64_t *, float *, cudaStream_t);
 int router_backward(const float *, const int64_t *, const float *, int64_t, int, int, int, float *, cudaStream_t);
+int router_gate(const void *, int, const float *, int64_t, int, int, int, int, float *, int64_t *, float *,
+                cudaStream_t);
 bool tc_available();
 bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out);
 int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
@@ -99,6 +101,14 @@ int smoe_router_topk(const float *in, int64_t T, int32_t num_experts, int32_t k,
   REQUIRE(T >= 0, SMOE_EINVAL, "router_topk: T must be >= 0");
   REQUIRE(T == 0 || (in && expert_idx && p), SMOE_EINVAL, "router_topk: null pointer");
   return router_topk(in, T, num_experts, k, apply_softmax, renormalize, gate_out, expert_idx, p, S(stream));
+}
+
+int smoe_router_gate(const void *x, int32_t x_dtype, const float *w_gate, int64_t T, int32_t d_model,
+                     int32_t num_experts, int32_t k, int32_t renormalize, float *gate_out, int64_t *expert_idx,
+                     float *p, void *stream) {
+  REQUIRE(T >= 0 && d_model >= 1, SMOE_EINVAL, "router_gate: T must be >= 0 and d_model >= 1");
+  REQUIRE(T == 0 || (x && w_gate && expert_idx && p), SMOE_EINVAL, "router_gate: null pointer");
+  return router_gate(x, x_dtype, w_gate, T, d_model, num_experts, k, renormalize, gate_out, expert_idx, p, S(stream));
 }
 
 int smoe_router_backward(const float *gate, const int64_t *expert_idx, const float *grad_p, int64_t T,

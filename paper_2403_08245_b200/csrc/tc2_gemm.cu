@@ -263,35 +263,35 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             // the leader also expects the peer's 16-byte relay signal
             mbar_expect_tx(fb, (GA ? 0 : A_BYTES) + (GB ? 0 : B_BYTES) + (leader ? 16 : 0));
             if (!GB) {
-              tma_load_2d(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
-              tma_load_2d(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
+              tma_load_2d_h(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk), p.pol_b);
+              tma_load_2d_h(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk), p.pol_b);
             }
             if (!GA) {
-              tma_load_2d(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
-              tma_load_2d(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+              tma_load_2d_h(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk), p.pol_a);
+              tma_load_2d_h(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk), p.pol_a);
             }
           } else if (RELAY) {
             // gather mode: this CTA's bytes are counted locally; the leader also
             // expects the peer's 16-byte relay signal on the same barrier
             mbar_expect_tx(fb, B_BYTES + TG_ROWS * 128 + (leader ? 16 : 0));
             if (BMODE == B_W_MN) {
-              tma_load_3d(&tma_b, fb, sb, n_half, kk, tl.e);
-              tma_load_3d(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
+              tma_load_3d_h(&tma_b, fb, sb, n_half, kk, tl.e, p.pol_b);
+              tma_load_3d_h(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e, p.pol_b);
             } else {
-              tma_load_3d(&tma_b, fb, sb, kk, n_half, tl.e);
+              tma_load_3d_h(&tma_b, fb, sb, kk, n_half, tl.e, p.pol_b);
             }
           } else if (GK && AM == A_MN && tl.k_len - kk < BK) {
             // bin-tail stage of a grouped-K tile: each CTA counts its own bytes
             // locally, zeroes its rows past the bin, and the peer then signals
             // the leader (see the tail fixer below)
             mbar_expect_tx(fb, B_BYTES + a_bytes + (leader ? 16 : 0));
-            tma_load_2d(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
-            tma_load_2d(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
-            tma_load_2d(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
-            tma_load_2d(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+            tma_load_2d_h(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk), p.pol_b);
+            tma_load_2d_h(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk), p.pol_b);
+            tma_load_2d_h(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk), p.pol_a);
+            tma_load_2d_h(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk), p.pol_a);
             if (bot) {
-              tma_load_2d(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk));
-              tma_load_2d(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk));
+              tma_load_2d_h(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk), p.pol_a);
+              tma_load_2d_h(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk), p.pol_a);
             }
           } else if (p.timing == 5 && it > 0) {
             // energy probe (SMOE_TC_TIMING=5, debug): after the first tile no
@@ -301,23 +301,23 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             // both CTAs' bytes are counted on the leader's barrier
             if (leader) mbar_expect_tx(fb, 2 * (B_BYTES + a_bytes));
             if (BMODE == B_W_MN) {
-              tma_load_3d_cg2(&tma_b, fb, sb, n_half, kk, tl.e);
-              tma_load_3d_cg2(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e);
+              tma_load_3d_cg2_h(&tma_b, fb, sb, n_half, kk, tl.e, p.pol_b);
+              tma_load_3d_cg2_h(&tma_b, fb, sb + 8192, n_half + 64, kk, tl.e, p.pol_b);
             } else if (BMODE == B_W_K) {
-              tma_load_3d_cg2(&tma_b, fb, sb, kk, n_half, tl.e);
+              tma_load_3d_cg2_h(&tma_b, fb, sb, kk, n_half, tl.e, p.pol_b);
             } else {
-              tma_load_2d_cg2(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk));
-              tma_load_2d_cg2(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk));
+              tma_load_2d_cg2_h(&tma_b, fb, sb, n_half, (int)(tl.k0 + kk), p.pol_b);
+              tma_load_2d_cg2_h(&tma_b, fb, sb + 8192, n_half + 64, (int)(tl.k0 + kk), p.pol_b);
             }
             if (AM == A_ROWS) {
-              tma_load_2d_cg2(&tma_a, fb, sa, (int)(tl.k0 + kk), m_half);
-              if (bot) tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES, (int)(tl.k0 + kk), m_half + TM);
+              tma_load_2d_cg2_h(&tma_a, fb, sa, (int)(tl.k0 + kk), m_half, p.pol_a);
+              if (bot) tma_load_2d_cg2_h(&tma_a, fb, sa + A_BYTES, (int)(tl.k0 + kk), m_half + TM, p.pol_a);
             } else if (AM == A_MN) {
-              tma_load_2d_cg2(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk));
-              tma_load_2d_cg2(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk));
+              tma_load_2d_cg2_h(&tma_a, fb, sa, m_half, (int)(tl.k0 + kk), p.pol_a);
+              tma_load_2d_cg2_h(&tma_a, fb, sa + 8192, m_half + 64, (int)(tl.k0 + kk), p.pol_a);
               if (bot) {
-                tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk));
-                tma_load_2d_cg2(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk));
+                tma_load_2d_cg2_h(&tma_a, fb, sa + A_BYTES, m_half + TM, (int)(tl.k0 + kk), p.pol_a);
+                tma_load_2d_cg2_h(&tma_a, fb, sa + A_BYTES + 8192, m_half + TM + 64, (int)(tl.k0 + kk), p.pol_a);
               }
             }
           }
@@ -986,6 +986,28 @@ static uint32_t *tile_counter(cudaStream_t st) {
   return c;
 }
 
+// L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: keep (default) |
+// keepfirst | off).  A raster band is group_m row-blocks x all column blocks,
+// visited row-block-fastest.  When a band holds more tiles than the 74
+// concurrent CTA pairs, a tile wave sweeps the band's columns and every wave
+// re-reads the band's A panels: A is kept (EVICT_LAST).  When the band is
+// smaller than a wave, each wave spans whole bands and it is the B panels
+// (weights / the grouped-K right operand) that the next bands re-read: B is kept.
+static void set_l2_policy(Params &q, int clusters, int tn) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char *env = getenv("SMOE_L2_HINT");
+    mode = !env ? 1 : !strcmp(env, "off") ? 0 : !strcmp(env, "keepfirst") ? 2 : 1;
+  }
+  q.pol_a = q.pol_b = kL2EvictNormal;
+  if (mode == 0) return;
+  const int64_t n_blocks = (q.N + tn - 1) / tn;
+  const bool a_persists = (int64_t)q.group_m * n_blocks > clusters;
+  const uint64_t other = mode == 2 ? kL2EvictFirst : kL2EvictNormal;
+  q.pol_a = a_persists ? kL2EvictLast : other;
+  q.pol_b = a_persists ? other : kL2EvictLast;
+}
+
 template <int AM, int BMODE, bool GK, bool STAGED, bool WIDE = false>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &tc, const CUtensorMap &tc2,
                   const Params &p, int64_t max_tiles, cudaStream_t st) {
@@ -1000,6 +1022,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   int clusters = num_sms() / 2;
   if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
   Params q = p;
+  set_l2_policy(q, clusters, TN);
   q.tile_ctr = tile_counter(st);
   if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
   kern<<<2 * clusters, kernel_threads(AM, BMODE), smem, st>>>(ta, tb, tc, tc2, q);

@@ -49,6 +49,7 @@ struct Params {
   float *dp_part;          // EPI_ACT_GRAD_SCALED: [M, dp_parts] partial dot products
   int dp_parts;
   int wide_defer;          // tc2 wide tiles: stages per first / last MMA group
+  uint64_t pol_a, pol_b;   // tc2 TMA loads: L2 eviction-priority policy per operand
 };
 
 __device__ __forceinline__ bool epi_scaled(int epi) {
@@ -70,17 +71,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// mbarrier waits carry a suspend-time hint: a waiting warp is parked until the
+// phase completes (or the hint, in ns, expires and the loop re-tries) instead
+// of re-issuing try_wait.  Without it the epilogue warps, waiting out a whole
+// tile's mainloop, were 65 % of a GEMM's executed warp instructions
+// (profiles/r1_wide_tiles.txt) — issue energy the 1 kW power cap takes out of
+// the clock.  SMOE_WAIT_HINT=0 builds the hint-free spin (A/B).
+#ifndef SMOE_WAIT_HINT
+#define SMOE_WAIT_HINT 0x989680
+#endif
+#if SMOE_WAIT_HINT
+#define SMOE_TRY_WAIT(scope) "mbarrier.try_wait.parity" scope ".shared::cta.b64 P1, [%0], %1, %2;\n"
+#else
+#define SMOE_TRY_WAIT(scope) "mbarrier.try_wait.parity" scope ".shared::cta.b64 P1, [%0], %1;\n"
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      SMOE_TRY_WAIT("")
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "n"(SMOE_WAIT_HINT)
       : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init() {
@@ -198,12 +213,12 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t par
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      SMOE_TRY_WAIT(".acquire.cluster")
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "n"(SMOE_WAIT_HINT)
       : "memory");
 }
 // release-arrive (cluster scope) on the barrier at this offset in CTA `cta`
@@ -257,12 +272,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      SMOE_TRY_WAIT("")
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "n"(SMOE_WAIT_HINT)
       : "memory");
 }
 __device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -434,6 +449,44 @@ __device__ __forceinline__ void tma_load_3d_cg2(const CUtensorMap *map, uint32_t
   asm volatile(
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar & kPeerBitMask)
+      : "memory");
+}
+// The same loads with an L2 eviction-priority hint (createpolicy encodings, as
+// CUTLASS's TMA::CacheHintSm90): the operand a raster band re-reads across
+// tile waves is kept (EVICT_LAST), the one consumed within a wave goes first.
+constexpr uint64_t kL2EvictNormal = 0x1000000000000000ull;
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ void tma_load_2d_cg2_h(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                                  uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar & kPeerBitMask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_cg2_h(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                                  int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar & kPeerBitMask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_h(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_h(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1,
+                                              int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
 // Zero K rows [valid, 64) of `boxes` MN-major 64-row boxes in the PEER CTA's

@@ -205,6 +205,38 @@ def gate_forward(x: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
     return _softmax_rows64(logits).to(torch.float32)
 
 
+def gate_topk(x: torch.Tensor, w_g: torch.Tensor, k: int, renormalize: bool = True) -> RoutingResult:
+    """topk_select(gate_forward(x, w_g), k) as one kernel (router.py:119-151).
+
+    csrc/router.cu router_gate_kernel: the gate GEMM accumulated in float64 (the
+    logits are never rounded), softmax in float64 rounded once to float32, the
+    stable top-k on the float32 gates and the float64 renormalisation; the ids
+    it writes go straight to compute_grouped_order.  x: (T, d_model) bf16 or
+    float32 CUDA tensor; w_g: (d_model, E), used in float32.
+    """
+    require_dims(x.dim() == 2 and w_g.dim() == 2 and x.shape[1] == w_g.shape[0], "gate matmul", tuple(x.shape),
+                 tuple(w_g.shape))
+    t, e = x.shape[0], w_g.shape[1]
+    if not 1 <= k <= e:
+        raise ValueError(f"k must be in [1, E]; got k={k}, E={e}")
+    if not x.is_cuda:
+        raise ValueError("x must be a CUDA tensor (there is no CPU path)")
+    if x.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError(f"x must be bfloat16 or float32, got {x.dtype}")
+    x = x.contiguous()
+    wg = w_g.to(device=x.device, dtype=torch.float32).contiguous()
+    gate = torch.empty((t, e), dtype=torch.float32, device=x.device)
+    idx = torch.empty((t, k), dtype=torch.int64, device=x.device)
+    p = torch.empty((t, k), dtype=torch.float32, device=x.device)
+    t0 = _lt.begin()
+    st = _lib.load().smoe_router_gate(x.data_ptr(), _lib.SMOE_BF16 if x.dtype == torch.bfloat16 else _lib.SMOE_F32,
+                                      wg.data_ptr(), t, x.shape[1], e, k, int(renormalize), gate.data_ptr(),
+                                      idx.data_ptr(), p.data_ptr(), _stream_ptr(x.device))
+    _lt.end("router_gate", t0)
+    _lib.check(st, "gate_topk")
+    return RoutingResult(expert_idx=idx, p=p, gate_full=gate, renormalized=renormalize, validate=False)
+
+
 def softmax_rows(logits: torch.Tensor) -> torch.Tensor:
     """Stable row softmax (router.py:126-128)."""
     return _softmax_rows64(logits.to(torch.float64)).to(logits.dtype)

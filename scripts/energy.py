@@ -42,6 +42,12 @@ MODES = {
     "dx": lambda: sm.scatter2scatter(h, w, order, 1, sm.GROUPED_TO_SCATTERED, transpose_w=True, out=xg),
     "xty": lambda: sm.group_xty(h, xg, order),
     "cublas": lambda: torch.matmul(xg, w[0]),   # dense reference: n x d @ d x d_e (same FLOPs as one GEMM)
+    "cublas_dw": lambda: torch.matmul(xg.t(), h),   # dense dW-shaped reference: d x n @ n x d_e (K = n)
+    "cublas_l2": lambda: torch.matmul(h, w.view(E, de, d)[0]),   # n x d_e @ d_e x d (K = d_e)
+    # torch's grouped GEMM (vendor kernels) on the exact grouped problems: layer 2 (K = d_e)
+    # and the grouped-input K = d GEMM, expert bins from the same routing
+    "gmm_l2": lambda: torch._grouped_mm(h, w.view(E, de, d), offs=order.bin_offsets[1:]),
+    "gmm_rows": lambda: torch._grouped_mm(xg, w, offs=order.bin_offsets[1:]),
 }
 
 
