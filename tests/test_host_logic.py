@@ -117,7 +117,8 @@ def test_mac_counter_is_padding_free_arithmetic():
 
 
 def test_bench_reference_arm_json_line():
-    """bench.py --impl reference (the oracle port on the host CPU) prints the
+    """bench.py --impl reference (the unmodified reference from baseline/_ref on the
+    host CPU; the oracle port only when baseline/_ref is absent) prints the
     contract's JSON line: metric/unit/higher_is_better, impl, cpu_baseline and
     an e2e object with zero transfer bytes; under torchrun only rank 0 prints."""
     import json
@@ -134,7 +135,9 @@ def test_bench_reference_arm_json_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["higher_is_better"] is True
-    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    from baseline import cpu_reference
+    want_kind = "reference" if cpu_reference.available() else "port"
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == want_kind and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     env = dict(__import__("os").environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     out1 = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "C0",
