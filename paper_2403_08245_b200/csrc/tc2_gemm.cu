@@ -986,18 +986,21 @@ static uint32_t *tile_counter(cudaStream_t st) {
   return c;
 }
 
-// L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: keep (default) |
-// keepfirst | off).  A raster band is group_m row-blocks x all column blocks,
+// L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: off (default) |
+// keep | keepfirst).  A raster band is group_m row-blocks x all column blocks,
 // visited row-block-fastest.  When a band holds more tiles than the 74
 // concurrent CTA pairs, a tile wave sweeps the band's columns and every wave
 // re-reads the band's A panels: A is kept (EVICT_LAST).  When the band is
 // smaller than a wave, each wave spans whole bands and it is the B panels
 // (weights / the grouped-K right operand) that the next bands re-read: B is kept.
+// Measured at C1 under the power cap (profiles/r2_l2_hint_ab.log): "keep" leaves
+// DRAM bytes and J per launch unchanged (l2 9.26 -> 9.25 GB), "keepfirst" adds
+// 4-6 GB of DRAM reads and costs 4 % — so the default issues no hint.
 static void set_l2_policy(Params &q, int clusters, int tn) {
   static int mode = -1;
   if (mode < 0) {
     const char *env = getenv("SMOE_L2_HINT");
-    mode = !env ? 1 : !strcmp(env, "off") ? 0 : !strcmp(env, "keepfirst") ? 2 : 1;
+    mode = (!env || !strcmp(env, "off")) ? 0 : !strcmp(env, "keepfirst") ? 2 : 1;
   }
   q.pol_a = q.pol_b = kL2EvictNormal;
   if (mode == 0) return;
