@@ -308,6 +308,8 @@ def run_ours(args, rank, world, local_rank):
             ev_steps[i].record(st)
         e1.record(st)
     torch.cuda.synchronize()
+    if ep_mode == "peer":
+        ep.check()   # the EP layer's only host read: timeouts / capacity overflow of the timed steps
     # memory of the timed steps alone (before the e2e / roofline sections allocate more)
     peak_step_bytes = torch.cuda.max_memory_allocated(dev)
     step_ms = sorted([e0.elapsed_time(ev_steps[0])] +

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SMOE_ABI_VERSION 3
+#define SMOE_ABI_VERSION 4
 
 typedef enum {
   SMOE_OK = 0,
@@ -113,6 +113,11 @@ int smoe_route_sort(const int64_t *expert_idx, int64_t n, int32_t num_experts,
  */
 int smoe_router_topk(const float *in, int64_t T, int32_t num_experts, int32_t k, int32_t apply_softmax,
                      int32_t renormalize, float *gate_out, int64_t *expert_idx, float *p, void *stream);
+/* SMs the persistent tcgen05 GEMMs leave free for kernels running concurrently
+ * on other streams (e.g. NCCL all-to-all chunks overlapping an expert GEMM);
+ * rounded down to whole CTA pairs; default 0.  Process-wide. */
+int smoe_set_sm_reserve(int32_t sms);
+
 /* Gate GEMM fused into the router (router.py:119-151):
  * logits = x @ w_gate accumulated in float64 (never rounded), softmax in float64
  * rounded once to float32 (gate_out [T, E], may be NULL), stable top-k on the
@@ -265,38 +270,67 @@ int smoe_ipc_get_handle(const void *dev_ptr, void *handle_out /* host, smoe_ipc_
 int smoe_ipc_open(const void *handle /* host */, void **dev_ptr_out /* host */);
 int smoe_ipc_close(void *dev_ptr /* the base smoe_ipc_open returned */);
 
-/* Dispatch: grouped row i of this rank (global expert e = sorted_expert[i],
- * owner q = e / experts_per_rank) is stored at row dstart[e] + i - bin_offsets[e]
- * of peer_rows[q]: x[order[i] / fan_out] (* weights[order[i]] if weights != NULL,
- * the p-weighted group of parallel_linear.py:213).  With peer_slot/peer_src the
- * row's slot id and this rank id are stored alongside (forward dispatch), with
- * slot_p/peer_p its routing weight slot_p[order[i]]. */
+/* Dispatch: grouped row i of this rank in global expert e's bin (owner
+ * q = e / experts_per_rank, num_experts = experts_per_rank * world) is stored at
+ * row j = dstart[e] + i - bin_offsets[e] of peer_rows[q]: x[order[i] / fan_out]
+ * (* weights[order[i]] if weights != NULL, the p-weighted group of
+ * parallel_linear.py:213).  With peer_slot/peer_src the row's slot id and this
+ * rank id are stored alongside (forward dispatch), with slot_p/peer_p its
+ * routing weight slot_p[order[i]].  Experts are sent in (local expert, owner)
+ * order; after each chunk of rows the sender fences at system scope and adds
+ * the chunk's row count to peer_arrive[q][e % experts_per_rank] (uint64, may be
+ * NULL), the owner's arrival gate.  Rows with j >= capacity are not written and
+ * set bit 2 of *err (device int32). */
 int smoe_ep_dispatch_rows(const void *x, int64_t x_rows, int64_t d, const int32_t *order,
-                          const int32_t *sorted_expert, const int32_t *bin_offsets, int32_t fan_out,
-                          const float *weights, int64_t n, const int64_t *dstart, int32_t experts_per_rank,
-                          const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src,
-                          int32_t me, const float *slot_p, const uint64_t *peer_p, int32_t dtype, void *stream);
-/* dp of received row j = sum of dp_part[j, :] (smoe_scatter2scatter_scaled
- * partials), stored at peer_dp[recv_src[j]][recv_slot[j]] (float). */
+                          const int32_t *bin_offsets, int32_t num_experts, int32_t fan_out, const float *weights,
+                          int64_t n, const int64_t *dstart, int32_t experts_per_rank, int32_t world,
+                          const uint64_t *peer_rows, const uint64_t *peer_slot, const uint64_t *peer_src, int32_t me,
+                          const float *slot_p, const uint64_t *peer_p, int64_t capacity, const uint64_t *peer_arrive,
+                          int32_t *err, int32_t dtype, void *stream);
+/* Sets bit 2 of *err when local_offsets[experts_per_rank] (rows routed to this
+ * rank) exceeds capacity (device-side; no host synchronisation). */
+int smoe_ep_check_capacity(const int32_t *local_offsets, int32_t experts_per_rank, int64_t capacity, int32_t *err,
+                           void *stream);
+/* The owner's expert GEMM on rows delivered by peers (grouped in, grouped out,
+ * bf16 tcgen05 CTA-pair engine): smoe_scatter2scatter_scaled's two epilogues
+ * (row scale s_i = row_scale[order[i]]; order is the identity [0, n) for rows
+ * in receive order) with each tile of local expert e started only
+ * once arrive[e] (see smoe_ep_dispatch_rows) reaches the expert's bin length
+ * local_offsets[e + 1] - local_offsets[e] — the dispatch overlaps the GEMM. */
+int smoe_ep_expert_gemm_gated(const void *x, int64_t n, const void *w, int32_t num_experts, int64_t w_rows,
+                              int64_t w_cols, const int32_t *order, const int32_t *local_offsets, int32_t transpose_w,
+                              int32_t epilogue,
+                              int32_t activation, const float *row_scale, void *out, void *out2, const void *aux,
+                              float *dp_part, int32_t dp_parts, const uint64_t *arrive, void *stream);
+/* group_xty (dw[e] = xg[bin e]^T yg[bin e]) whose yg rows are delivered by
+ * peers: each tile of expert e waits for arrive_y[e] as above. */
+int smoe_ep_group_xty_gated(const void *xg, const void *yg, const int32_t *local_offsets, int32_t num_experts,
+                            int64_t n, int64_t d_in, int64_t d_out, void *dw, const uint64_t *arrive_y, void *stream);
+/* dp of received row j < n_valid (= *n_valid, device, may be NULL for n) = sum
+ * of dp_part[j, :] (smoe_scatter2scatter_scaled partials), stored at
+ * peer_dp[recv_src[j]][recv_slot[j]] (float). */
 int smoe_ep_dp_return(const float *dp_part, int64_t n, int32_t parts, const int32_t *recv_slot,
-                      const int32_t *recv_src, const uint64_t *peer_dp, void *stream);
-/* Return: local row j goes to row recv_slot[j] of peer_out[recv_src[j]]. */
+                      const int32_t *recv_src, const uint64_t *peer_dp, const int32_t *n_valid, void *stream);
+/* Return: local row j < n_valid goes to row recv_slot[j] of peer_out[recv_src[j]]. */
 int smoe_ep_return_rows(const void *y, int64_t n, int64_t d, const int32_t *recv_slot, const int32_t *recv_src,
-                        const uint64_t *peer_out, int32_t dtype, void *stream);
+                        const uint64_t *peer_out, const int32_t *n_valid, int32_t dtype, void *stream);
 /* The return fused into the expert GEMM: out_j = x_j @ W[e] (or W[e]^T) for the
- * grouped rows x [n, d_in] (bins = expert_offsets), each output row stored by
- * the GEMM epilogue straight into row recv_slot[j] of peer_out[recv_src[j]]
- * (bf16, tcgen05 CTA-pair engine). */
+ * grouped rows x [n, d_in] (bins = expert_offsets; rows past the last bin are
+ * never touched), each output row stored by the GEMM epilogue straight into row
+ * recv_slot[j] of peer_out[recv_src[j]] (bf16, tcgen05 CTA-pair engine). */
 int smoe_ep_gemm_return(const void *x, int64_t n, const void *w, int32_t num_experts, int64_t w_rows, int64_t w_cols,
                         const int32_t *expert_offsets, int32_t transpose_w, const int32_t *recv_slot,
                         const int32_t *recv_src, const uint64_t *peer_out, void *stream);
 /* Copy `bytes` from src to every peer_dst[q] + offset_bytes. */
 int smoe_ep_put(const void *src, int64_t bytes, const uint64_t *peer_dst, int64_t offset_bytes, int32_t world,
                 void *stream);
-/* Signal every peer (system fence, then +1 on peer q's flags[slot * world + me]) /
- * wait until flags[slot * world + s] >= target for every source s (err = 1 on timeout). */
-int smoe_ep_signal(const uint64_t *peer_flags, int32_t world, int32_t me, int32_t slot, void *stream);
-int smoe_ep_wait(const uint64_t *flags, int32_t world, int32_t slot, uint64_t target, int64_t timeout_ns,
+/* Signal every peer (system fence, then +1 on peer q's flags[slot * world + me],
+ * and +1 on this rank's my_epochs[slot]) / wait until flags[slot * world + s]
+ * >= my_epochs[slot] for every source s (bit 1 of *err on timeout).  Epochs live
+ * on the device, so a signal / wait sequence replays inside a CUDA graph. */
+int smoe_ep_signal(const uint64_t *peer_flags, int32_t world, int32_t me, int32_t slot, uint64_t *my_epochs,
+                   void *stream);
+int smoe_ep_wait(const uint64_t *flags, int32_t world, int32_t slot, const uint64_t *my_epochs, int64_t timeout_ns,
                  int32_t *err, void *stream);
 
 #ifdef __cplusplus

@@ -37,6 +37,7 @@ SIGNATURES = {
     "smoe_route_sort": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "smoe_router_topk": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smoe_router_backward": (_c.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_set_sm_reserve": (_c.c_int, [_i32]),
     "smoe_router_gate": (_c.c_int, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smoe_scatter2scatter": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
                                         _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
@@ -50,10 +51,14 @@ SIGNATURES = {
     "smoe_ipc_get_handle": (_c.c_int, [_vp, _vp, _c.POINTER(_c.c_int64)]),
     "smoe_ipc_open": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p)]),
     "smoe_ipc_close": (_c.c_int, [_vp]),
-    "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _vp, _vp, _vp,
-                                         _i32, _vp, _vp, _i32, _vp]),
-    "smoe_ep_dp_return": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
-    "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "smoe_ep_dispatch_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp, _i32, _i32, _vp,
+                                         _vp, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _i32, _vp]),
+    "smoe_ep_check_capacity": (_c.c_int, [_vp, _i32, _i64, _vp, _vp]),
+    "smoe_ep_expert_gemm_gated": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
+                                             _vp, _vp, _vp, _i32, _vp, _vp]),
+    "smoe_ep_group_xty_gated": (_c.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "smoe_ep_dp_return": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "smoe_ep_return_rows": (_c.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp]),
     "smoe_scatter2scatter_scaled": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
                                                _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "smoe_dp_parts": (_i32, [_i64]),
@@ -62,8 +67,8 @@ SIGNATURES = {
     "smoe_dp_from_partials": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "smoe_ep_gemm_return": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "smoe_ep_put": (_c.c_int, [_vp, _i64, _vp, _i64, _i32, _vp]),
-    "smoe_ep_signal": (_c.c_int, [_vp, _i32, _i32, _i32, _vp]),
-    "smoe_ep_wait": (_c.c_int, [_vp, _i32, _i32, _c.c_uint64, _i64, _vp, _vp]),
+    "smoe_ep_signal": (_c.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "smoe_ep_wait": (_c.c_int, [_vp, _i32, _i32, _vp, _i64, _vp, _vp]),
     "smoe_group_xty_scattered": (_c.c_int, [_vp, _i64, _i32, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _i64,
                                             _i64, _i64, _i32, _vp, _i32, _vp]),
     "smoe_scatter_combine": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32,
@@ -78,7 +83,7 @@ class LibraryError(RuntimeError):
     """The native library is missing or a native call failed."""
 
 
-ABI_VERSION = 3  # include/smoe_b200.h SMOE_ABI_VERSION
+ABI_VERSION = 4  # include/smoe_b200.h SMOE_ABI_VERSION
 
 
 def load(path: str | os.PathLike | None = None):

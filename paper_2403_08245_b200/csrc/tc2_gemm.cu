@@ -249,6 +249,12 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
 #pragma unroll
         for (int j = 0; j < 4; ++j) gr[j] = __ldg(p.order + min((int64_t)m_half + 4 * lane + j, tl.m_end - 1)) / p.fan_out;
       }
+      // expert parallelism: the tile's input rows were stored by peers — wait
+      // until every row of this expert has arrived (grouped inputs only)
+      if (p.arrive && tl.nkb > 0) {
+        if (elect_one_sync()) arrival_gate(p.arrive, tl.e, (int64_t)s_off[tl.e + 1] - s_off[tl.e]);
+        __syncwarp();
+      }
       for (int kb = 0; kb < tl.nkb; ++kb) {
         const uint32_t fb = smem_u32(&lfull_bar[stage]);
         const uint32_t sa = smem_u32(tiles_smem + stage * SBYTES);
@@ -599,10 +605,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         const bool combine = p.epi == EPI_COMBINE;
         // *_SCALED epilogues: this thread's row scale and combine-weight-gradient partial
         float rscale = 1.0f, dpacc = 0.0f;
-        if (epi_scaled(p.epi) && dst >= 0) rscale = __ldg(p.pw + p.order[row]);
+        if (epi_scaled(p.epi) && dst >= 0) rscale = __ldcg(p.pw + p.order[row]);
         float cscale = 0.f;  // combine: this thread's row weight; cdst becomes the token row
         if (combine) {
-          if (dst >= 0) cscale = __ldg(p.pw + dst);
+          if (dst >= 0) cscale = __ldcg(p.pw + dst);
   #pragma unroll
           for (int i = 0; i < 8; ++i) cdst[i] = cdst[i] >= 0 ? cdst[i] / p.combine_cols : -1;
         }
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
         const bool use_aux = epi_act_grad(p.epi) && valid;
         float rscale = 1.0f, dpacc = 0.0f;
-        if (epi_scaled(p.epi) && valid) rscale = __ldg(p.pw + p.order[row]);
+        if (epi_scaled(p.epi) && valid) rscale = __ldcg(p.pw + p.order[row]);
         if (use_aux) {
           const int64_t c0 = tl.n0 + c_begin;
   #pragma unroll
@@ -972,6 +978,25 @@ bool tc2_supports_experts(int E) {
 
 namespace tc2 {
 
+// SMs the persistent GEMMs leave free (smoe_set_sm_reserve): a GEMM occupies
+// one CTA per SM with ~230 KB of shared memory, so a kernel that must run
+// concurrently with it on another stream (NCCL's all-to-all in ep.py) needs
+// SMs of its own.
+static std::atomic<int> g_sm_reserve{0};
+static int sm_reserve() { return g_sm_reserve.load(std::memory_order_relaxed); }
+
+}  // namespace tc2
+}  // namespace smoe
+
+extern "C" int smoe_set_sm_reserve(int32_t sms) {
+  if (sms < 0 || sms > smoe::num_sms() - 2) return smoe::fail(SMOE_EINVAL, "sm_reserve out of range");
+  smoe::tc2::g_sm_reserve.store(sms & ~1, std::memory_order_relaxed);   // whole CTA pairs
+  return SMOE_OK;
+}
+
+namespace smoe {
+namespace tc2 {
+
 // Tile counters of the dynamic schedule: one zeroed (stream-ordered memset) per
 // launch; a 64-entry pool so launches in flight on different streams never
 // share one.
@@ -1022,7 +1047,8 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
       return check_launch("tc2_gemm: smem attribute");
     configured = smem;
   }
-  int clusters = num_sms() / 2;
+  int clusters = (num_sms() - sm_reserve()) / 2;
+  if (clusters < 1) clusters = 1;
   if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
   Params q = p;
   set_l2_policy(q, clusters, TN);
@@ -1126,7 +1152,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
                     int epi, int act, void *out, void *out2, const void *aux, const float *pw, float *yacc,
                     int combine_cols, cudaStream_t st, const uint64_t *peer_out = nullptr,
                     const int32_t *row_src = nullptr, const int32_t *row_slot = nullptr,
-                    float *dp_part = nullptr, int dp_parts = 0) {
+                    float *dp_part = nullptr, int dp_parts = 0, const unsigned long long *arrive = nullptr) {
   const int64_t d_in = trans ? w_cols : w_rows;
   const int64_t d_out = trans ? w_rows : w_cols;
   CUtensorMap ta, tb;
@@ -1167,6 +1193,7 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.combine_cols = combine_cols;
   p.group_m = band_rows(d_in);
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
+  p.arrive = arrive;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
   CUtensorMap tc = ta, tc2 = ta;  // unused unless the output is grouped
   if (gout) {
@@ -1208,6 +1235,16 @@ int scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int E, 
                   aux, row_scale, nullptr, 1, st, nullptr, nullptr, nullptr, dp_part, dp_parts);
 }
 
+// The scaled epilogues on rows delivered by peers (expert parallelism): grouped
+// in / grouped out, each tile gated on its expert's arrival counter.
+int scatter2scatter_scaled_gated(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                                 const int32_t *order, const int32_t *offsets, int64_t n, int trans, int epi, int act,
+                                 const float *row_scale, void *out, void *out2, const void *aux, float *dp_part,
+                                 int dp_parts, const unsigned long long *arrive, cudaStream_t st) {
+  return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, 1, 1, 1, trans, epi, act, out, out2, aux,
+                  row_scale, nullptr, 1, st, nullptr, nullptr, nullptr, dp_part, dp_parts, arrive);
+}
+
 // Grouped-input GEMM whose epilogue stores output row i straight into row
 // row_slot[i] of rank row_src[i]'s buffer (peer memory): the expert-parallel
 // return fused into the expert GEMM (ep_peer.py).
@@ -1230,7 +1267,7 @@ int scatter_combine(const void *x, int64_t x_rows, const void *w, int E, int64_t
 }
 
 int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in, int64_t d_out,
-              void *dw, cudaStream_t st) {
+              void *dw, cudaStream_t st, const unsigned long long *arrive) {
   CUtensorMap ta, tb;
   uint64_t rows = (uint64_t)(n > 0 ? n : 1);
   {
@@ -1257,6 +1294,7 @@ int group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int
   p.out = (__nv_bfloat16 *)dw;
   p.group_m = group_m_k_setting();
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
+  p.arrive = arrive;
   const int64_t max_tiles = (int64_t)E * ((d_in + TM - 1) / TM) * ((d_out + TN - 1) / TN);
   CUtensorMap tc;
   if (!encode_out_map(&tc, dw, (int64_t)E * d_in, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(dW) failed");

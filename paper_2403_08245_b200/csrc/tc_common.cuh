@@ -50,7 +50,24 @@ struct Params {
   int dp_parts;
   int wide_defer;          // tc2 wide tiles: stages per first / last MMA group
   uint64_t pol_a, pol_b;   // tc2 TMA loads: L2 eviction-priority policy per operand
+  // Expert-parallel arrival gate (grouped inputs written by peers): before
+  // loading a tile of local expert e the producer waits until arrive[e] (a
+  // peer-incremented row counter) reaches the expert's bin length.
+  const unsigned long long *arrive;
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait (one elected lane of the producer warp) until peers delivered every row
+// of expert e, then order those generic-proxy stores before this thread's
+// async-proxy (TMA) reads of them.
+__device__ __forceinline__ void arrival_gate(const unsigned long long *arrive, int e, int64_t need) {
+  while ((int64_t)ld_acquire_sys_u64(arrive + e) < need) __nanosleep(128);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 __device__ __forceinline__ bool epi_scaled(int epi) {
   return epi == SMOE_EPI_ACT_SCALED || epi == SMOE_EPI_ACT_GRAD_SCALED;

@@ -401,7 +401,8 @@ static inline bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 namespace tc2 {
 int scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
                     int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
-int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
+int group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t,
+              const unsigned long long *arrive = nullptr);
 int scatter_combine(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
                     int64_t, int, int, const float *, int, float *, cudaStream_t);
 int group_xty_scattered(const void *, int64_t, int, int, const void *, int64_t, int, int, const int32_t *,
@@ -412,6 +413,9 @@ int scatter2scatter_peer(const void *, int64_t, const void *, int, int64_t, int6
 int scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
                            const int32_t *, int64_t, int, int, int, int, int, int, const float *, void *, void *,
                            const void *, float *, int, cudaStream_t);
+int scatter2scatter_scaled_gated(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                                 const int32_t *, int64_t, int, int, int, const float *, void *, void *, const void *,
+                                 float *, int, const unsigned long long *, cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -538,6 +542,27 @@ int tc_group_xty_scattered(const void *x, int64_t x_rows, int fa, int ga, const 
     return fail(SMOE_ENOTSUP, "tcgen05 group_xty over scattered operands needs the CTA-pair engine, d_in, d_out "
                               "multiples of 8 and 16-byte aligned buffers");
   return tc2::group_xty_scattered(x, x_rows, fa, ga, y, y_rows, fb, gb, order, offsets, E, n, d_in, d_out, dw, st);
+}
+
+// Expert parallelism: GEMMs on rows stored by peers, each tile gated on its
+// expert's arrival counter (CTA-pair engine only).
+int tc_ep_scaled_gated(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                       const int32_t *order, const int32_t *offsets, int64_t n, int trans, int epi, int act,
+                       const float *row_scale, void *out, void *out2, const void *aux, float *dp_part, int dp_parts,
+                       const unsigned long long *arrive, cudaStream_t st) {
+  const int64_t d_in = trans ? w_cols : w_rows, d_out = trans ? w_rows : w_cols;
+  if (!(tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && tc_supports_s2s(d_in, d_out, x, w, out)))
+    return fail(SMOE_ENOTSUP, "gated expert GEMM needs the CTA-pair engine, d_in, d_out multiples of 8");
+  return tc2::scatter2scatter_scaled_gated(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, trans, epi, act,
+                                           row_scale, out, out2, aux, dp_part, dp_parts, arrive, st);
+}
+
+int tc_ep_group_xty_gated(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in,
+                          int64_t d_out, void *dw, const unsigned long long *arrive, cudaStream_t st) {
+  if (!(tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && d_in % 8 == 0 && d_out % 8 == 0 && al16(xg) &&
+        al16(yg) && al16(dw)))
+    return fail(SMOE_ENOTSUP, "gated group_xty needs the CTA-pair engine, d_in, d_out multiples of 8");
+  return tc2::group_xty(xg, yg, offsets, E, n, d_in, d_out, dw, st, arrive);
 }
 
 int tc_group_xty(const void *xg, const void *yg, const int32_t *offsets, int E, int64_t n, int64_t d_in,

@@ -6,17 +6,23 @@ ordered by source rank, then by the source's grouped order, so every result
 is bit-identical to one GPU running the concatenated batch), but no NCCL
 all-to-all and no pack / unpack copies:
 
-  forward   1. device barrier: every peer is done with the previous step's
-               buffers;
+  forward   1. each rank zeroes its arrival counters, then a device barrier:
+               every peer is done with the previous step's buffers;
             2. each rank stores its per-expert counts (E int64) into row `me`
-               of every peer's count table, signal + wait; one host read of the
-               table gives the receive sizes (the step's only host sync);
+               of every peer's count table, signal + wait; the receive layout
+               (dstart, local bin offsets) is computed from the table ON THE
+               DEVICE — no host synchronisation anywhere in the step, which
+               therefore captures into a CUDA graph;
             3. dispatch kernel: grouped row i of this rank goes straight to row
                dstart[e] + (i - off[e]) of the owner's receive buffer — its
                final position in the owner's local grouped order — together
-               with its slot id and the source rank;
-            4. the owner runs layer 1 on the received rows as they landed
-               (grouped in, grouped out: TMA-fed, no group() copy);
+               with its slot id, the source rank and its routing weight; experts
+               go out in (local expert, owner) order and every 64-row chunk
+               bumps the owner's arrival counter of that expert;
+            4. the owner runs layer 1 on the received rows as they land: each
+               GEMM tile of local expert e waits (in the TMA producer) for
+               e's arrival counter, so the dispatch of later experts overlaps
+               the first experts' GEMM (grouped in, grouped out, TMA-fed);
             5. layer 2's GEMM epilogue stores output row j straight into row
                slot[j] of its source's slot-ordered buffer (the combine-side
                all-to-all fused into the expert GEMM); the source combines
@@ -26,6 +32,13 @@ all-to-all and no pack / unpack copies:
             only (dW stays local: no all-reduce); the input-gradient GEMM's
             epilogue stores the slot gradients into the source's buffer, which
             reduces over the k slots.
+
+Receive buffers hold ``capacity`` rows: by default the exact worst case (every
+rank's rows on one owner, G*T*k), or ceil(capacity_factor * T * k) rows.  A
+step whose routing sends more rows to a rank than it can hold does not write
+past the buffer: the overflow bit of the device error word is set and
+``check()`` raises (``check()`` is the only host read; call it when a step's
+results are consumed, e.g. at logging intervals).
 
 Peer buffers are CUDA IPC mappings of each rank's buffers (``SymmetricBuffer``);
 the store kernels write through NVLink P2P on a multi-GPU box and into the
@@ -125,7 +138,6 @@ class PeerEpContext:
     p: torch.Tensor
     k: int
     dstart: torch.Tensor
-    n_recv: int
     order_loc: GroupedOrder
     h_pre: torch.Tensor
     h: torch.Tensor
@@ -170,7 +182,8 @@ class PeerExpertParallelSmoeMlp:
     """
 
     def __init__(self, w1_local, w2_local, num_experts: int, k: int, max_tokens: int, group=None,
-                 activation: str = "gelu", timeout_s: float = 60.0, scaled: bool | None = None):
+                 activation: str = "gelu", timeout_s: float = 60.0, scaled: bool | None = None,
+                 capacity_factor: float | None = None):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -183,6 +196,7 @@ class PeerExpertParallelSmoeMlp:
             raise ValueError("the peer-memory EP path runs the bf16 tensor-core kernels")
         self.w1, self.w2 = w1_local, w2_local
         self.num_experts, self.k, self.activation = num_experts, k, activation
+        self.e_local = el
         self.max_tokens = max_tokens
         self.timeout_ns = int(timeout_s * 1e9)
         # the routing weight travels with the row and moves through layer 2 at
@@ -192,10 +206,17 @@ class PeerExpertParallelSmoeMlp:
         self.scaled = moe_layers._SCALED if scaled is None else bool(scaled)
         dev = w1_local.device
         d = w1_local.shape[1]
+        de = w1_local.shape[2]
         self.d = d
         g = self.world
         slots = max_tokens * k
-        cap = slots * g                                  # worst case: all rows to one owner
+        worst = slots * g                                # every rank's rows on one owner
+        if capacity_factor is None:
+            cap = worst
+        else:
+            if capacity_factor <= 0:
+                raise ValueError(f"capacity_factor must be > 0, got {capacity_factor}")
+            cap = min(worst, -(-int(capacity_factor * slots) // 256) * 256)
         self.cap = cap
         esz = 2
         self.flags = SymmetricBuffer(8 * _NUM_SLOTS * g, dev, group)
@@ -208,8 +229,16 @@ class PeerExpertParallelSmoeMlp:
         self.dx_ret = SymmetricBuffer(esz * slots * d, dev, group)
         self.recv_p = SymmetricBuffer(4 * cap, dev, group)      # routing weight of each received row
         self.dp_ret = SymmetricBuffer(4 * slots, dev, group)    # dp per slot, returned by the owners
+        # arrival counters of the forward (x rows) and backward (dY rows) dispatch, E_l each
+        self.arrive = SymmetricBuffer(8 * 2 * el, dev, group)
+        self.arrive_bwd_peers = self.arrive.peers + 8 * el
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.epoch = [0] * _NUM_SLOTS
+        self.my_epochs = torch.zeros(_NUM_SLOTS, dtype=torch.int64, device=dev)
+        # persistent per-step buffers (no allocation inside the step)
+        self.h_pre = torch.empty((cap, de), dtype=torch.bfloat16, device=dev)
+        self.h = torch.empty_like(self.h_pre)
+        self.parts = torch.empty((cap, K.dp_parts(de)), dtype=torch.float32, device=dev) if self.scaled else None
+        self.o_loc = torch.arange(cap, dtype=torch.int32, device=dev)
         # every rank must have mapped every peer buffer; decide collectively so
         # all ranks raise together (a caller can then fall back to ep.py)
         errors = [b.error for b in self._buffers() if b.error]
@@ -222,24 +251,36 @@ class PeerExpertParallelSmoeMlp:
 
     # ---- completion ------------------------------------------------------------
     def _exchange_done(self, slot: int) -> None:
-        """Signal every peer for `slot`, then wait for every peer's signal."""
+        """Signal every peer for `slot`, then wait for every peer's signal (device-side epochs)."""
         lib = _lib.load()
-        self.epoch[slot] += 1
         t0 = _lt.begin()
-        _lib.check(lib.smoe_ep_signal(self.flags.peers.data_ptr(), self.world, self.rank, slot, _stream()),
-                   "ep_signal")
-        _lib.check(lib.smoe_ep_wait(self.flags.local.data_ptr(), self.world, slot, self.epoch[slot],
+        _lib.check(lib.smoe_ep_signal(self.flags.peers.data_ptr(), self.world, self.rank, slot,
+                                      self.my_epochs.data_ptr(), _stream()), "ep_signal")
+        _lib.check(lib.smoe_ep_wait(self.flags.local.data_ptr(), self.world, slot, self.my_epochs.data_ptr(),
                                     self.timeout_ns, self.err.data_ptr(), _stream()), "ep_wait")
         _lt.end(f"ep_sync {_SLOT_NAMES[slot]}", t0)
 
-    def _check_err(self) -> None:
-        if int(self.err.item()):
-            raise RuntimeError("peer-memory EP: a peer did not signal within the timeout")
+    def check(self) -> None:
+        """Raise if a step since the last check timed out waiting for a peer or overflowed
+        the receive capacity (the one host read of the layer; results of such a step are invalid)."""
+        code = int(self.err.item())
+        if code:
+            self.err.zero_()
+            why = []
+            if code & 1:
+                why.append("a peer did not signal within the timeout")
+            if code & 2:
+                why.append(f"more rows were routed to a rank than its receive capacity ({self.cap} rows); "
+                           f"raise capacity_factor (None = the exact worst case)")
+            raise RuntimeError("peer-memory EP: " + "; ".join(why))
+
+    _check_err = check
 
     # ---- forward / backward ------------------------------------------------------
     def forward(self, x: torch.Tensor, routing: RoutingResult):
         lib = _lib.load()
         k, g, e = routing.k, self.world, self.num_experts
+        el = self.e_local
         t = x.shape[0]
         if k != self.k or t > self.max_tokens:
             raise ValueError(f"routing k={k} / {t} tokens exceed the buffers (k={self.k}, max_tokens={self.max_tokens})")
@@ -248,37 +289,37 @@ class PeerExpertParallelSmoeMlp:
         x = x.contiguous()
         order = compute_grouped_order(routing, e)
         n = order.num_slots
-        # 1. previous step's buffers are free everywhere
+        # 1. this rank's arrival counters start from zero; then every peer is
+        #    done with the previous step's buffers (and has zeroed its counters)
+        self.arrive.local.zero_()
         self._exchange_done(_READY)
-        # 2. count table
+        # 2. count table -> receive layout, on the device
         cnt = order.bin_counts.to(torch.int64).contiguous()
         _call("ep_put counts", lib.smoe_ep_put, cnt.data_ptr(), 8 * e, self.counts.peers.data_ptr(),
               8 * e * self.rank, g, _stream())
         self._exchange_done(_COUNTS)
         table = self.counts.view(torch.int64, (g, e))
         dstart, off_loc = dispatch_layout(table, self.rank)
-        n_recv = int(off_loc[-1])                      # the one host sync of the step
-        self._check_err()
+        off32 = off_loc.clamp(max=self.cap).to(torch.int32)     # never past the receive buffer
+        _call("ep_check_capacity", lib.smoe_ep_check_capacity, off_loc.to(torch.int32).data_ptr(), el, self.cap,
+              self.err.data_ptr(), _stream())
+        order_loc = GroupedOrder(o=self.o_loc, bin_offsets=off32, validate=False)
         # 3. dispatch rows (+ slot ids, source rank, routing weight) to their owners
         pw = routing.p.reshape(-1).to(torch.float32).contiguous()
-        _call("ep_dispatch x", lib.smoe_ep_dispatch_rows,
-              x.data_ptr(), t, self.d, order.o.data_ptr(), order.sorted_expert_idxs.data_ptr(),
-              order.bin_offsets.data_ptr(), k, None, n, dstart.data_ptr(), e // g, self.recv_x.peers.data_ptr(),
-              self.recv_slot.peers.data_ptr(), self.recv_src.peers.data_ptr(), self.rank,
-              pw.data_ptr() if self.scaled else None, self.recv_p.peers.data_ptr() if self.scaled else None,
-              _lib.SMOE_BF16, _stream())
-        self._exchange_done(_FWD_DISPATCH)
-        # 4. local experts on the landed rows (grouped in, grouped out)
-        r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))[:n_recv]
-        order_loc = GroupedOrder(o=torch.arange(n_recv, dtype=torch.int32, device=x.device),
-                                 bin_offsets=off_loc.to(torch.int32), validate=False)
+        self._dispatch(x, order, k, None, dstart, self.recv_x, with_meta=True, pw=pw,
+                       arrive=self.arrive.peers if self.scaled else None, label="ep_dispatch x")
         de = self.w1.shape[2]
-        h_pre = torch.empty((n_recv, de), dtype=x.dtype, device=x.device)
-        h = torch.empty_like(h_pre)
-        if self.scaled:   # h = p * act(h_pre); order_loc is the identity, so row i's scale is recv_p[i]
-            K.scatter2scatter_scaled(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, row_scale=self._recv_p(n_recv),
-                                     activation=self.activation, out=h_pre, act_out=h)
+        r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))
+        h_pre, h = self.h_pre, self.h
+        if self.scaled:
+            # 4. h = p * act(h_pre) on the rows as they land: tiles gated on the arrival counters
+            _call("ep_expert_gemm_gated (layer 1)", lib.smoe_ep_expert_gemm_gated,
+                  r.data_ptr(), self.cap, self.w1.data_ptr(), el, self.w1.shape[1], de, self.o_loc.data_ptr(),
+                  off32.data_ptr(), 0,
+                  _lib.EPI_ACT_SCALED, _lib.ACTIVATION_IDS[self.activation], self._recv_p().data_ptr(),
+                  h_pre.data_ptr(), h.data_ptr(), None, None, 0, self.arrive.local.data_ptr(), _stream())
         else:
+            self._exchange_done(_FWD_DISPATCH)
             K.scatter2scatter(r, self.w1, order_loc, 1, GROUPED_TO_GROUPED, out=h_pre, activation=self.activation,
                               act_out=h)
         # 5. layer 2, its outputs stored back into their source slots; then the
@@ -287,38 +328,48 @@ class PeerExpertParallelSmoeMlp:
         self._exchange_done(_FWD_RETURN)
         y_slot = self.y_ret.view(torch.bfloat16, (self.max_tokens * k, self.d))[:n]
         y = K.fanout_reduce(y_slot, k) if self.scaled else K.combine(routing.p, y_slot)
-        ctx = PeerEpContext(order=order, p=routing.p, k=k, dstart=dstart, n_recv=n_recv, order_loc=order_loc,
+        ctx = PeerEpContext(order=order, p=routing.p, k=k, dstart=dstart, order_loc=order_loc,
                             h_pre=h_pre, h=h, y_slot=y_slot, activation=self.activation)
         return y, ctx
 
     def backward(self, ctx: PeerEpContext, dy: torch.Tensor) -> PeerEpGradients:
         lib = _lib.load()
         g, e, k = self.world, self.num_experts, ctx.k
+        el = self.e_local
         t = ctx.p.shape[0]
         dy = dy.contiguous()
         n = ctx.order.num_slots
         dp = None if self.scaled else K.combine_grad_p(dy, ctx.y_slot, t, k)
         pw = ctx.p.reshape(-1).to(torch.float32).contiguous()
-        # scaled form: unweighted dY rows (p is applied in the owner's dH epilogue)
-        _call("ep_dispatch dy", lib.smoe_ep_dispatch_rows,
-              dy.data_ptr(), t, self.d, ctx.order.o.data_ptr(), ctx.order.sorted_expert_idxs.data_ptr(),
-              ctx.order.bin_offsets.data_ptr(), k, None if self.scaled else pw.data_ptr(), n, ctx.dstart.data_ptr(),
-              e // g, self.recv_dy.peers.data_ptr(), None, None, self.rank, None, None, _lib.SMOE_BF16, _stream())
-        self._exchange_done(_BWD_DISPATCH)
-        nr = ctx.n_recv
-        dyl = self.recv_dy.view(torch.bfloat16, (self.cap, self.d))[:nr]
-        r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))[:nr]
         ol = ctx.order_loc
-        dw2 = K.group_xty(ctx.h, dyl, ol)
-        if self.scaled:   # dH = p * (dY W2^T) * act'(h_pre), dp partials from the same accumulators
-            parts = torch.empty((nr, K.dp_parts(self.w1.shape[2])), dtype=torch.float32, device=dy.device)
-            dh = K.scatter2scatter_scaled(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, row_scale=self._recv_p(nr),
-                                          activation=ctx.activation, out=ctx.h, act_grad_of=ctx.h_pre,
-                                          dp_partials=parts, transpose_w=True)
-            _call("ep_dp_return", lib.smoe_ep_dp_return, parts.data_ptr(), nr, parts.shape[1],
-                  self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr(), self.dp_ret.peers.data_ptr(),
+        off32 = ol.bin_offsets
+        # scaled form: unweighted dY rows (p is applied in the owner's dH epilogue)
+        self._dispatch(dy, ctx.order, k, None if self.scaled else pw, ctx.dstart, self.recv_dy, with_meta=False,
+                       arrive=self.arrive_bwd_peers if self.scaled else None, label="ep_dispatch dy")
+        dyl = self.recv_dy.view(torch.bfloat16, (self.cap, self.d))
+        r = self.recv_x.view(torch.bfloat16, (self.cap, self.d))
+        de = self.w1.shape[2]
+        if self.scaled:
+            arrive_bwd = self.arrive.local.data_ptr() + 8 * el
+            # dW2 = hp^T dY and dH = p * (dY W2^T) * act'(h_pre) (+ dp partials), each
+            # tile gated on the arrival of its expert's dY rows
+            dw2 = torch.empty((el, de, self.d), dtype=torch.bfloat16, device=dy.device)
+            _call("ep_group_xty_gated (dW2)", lib.smoe_ep_group_xty_gated, ctx.h.data_ptr(), dyl.data_ptr(),
+                  off32.data_ptr(), el, self.cap, de, self.d, dw2.data_ptr(), arrive_bwd, _stream())
+            parts = self.parts
+            _call("ep_expert_gemm_gated (dH)", lib.smoe_ep_expert_gemm_gated,
+                  dyl.data_ptr(), self.cap, self.w2.data_ptr(), el, de, self.d, self.o_loc.data_ptr(),
+                  off32.data_ptr(), 1,
+                  _lib.EPI_ACT_GRAD_SCALED, _lib.ACTIVATION_IDS[ctx.activation], self._recv_p().data_ptr(),
+                  ctx.h.data_ptr(), None, ctx.h_pre.data_ptr(), parts.data_ptr(), parts.shape[1], arrive_bwd,
                   _stream())
+            dh = ctx.h
+            _call("ep_dp_return", lib.smoe_ep_dp_return, parts.data_ptr(), self.cap, parts.shape[1],
+                  self.recv_slot.local.data_ptr(), self.recv_src.local.data_ptr(), self.dp_ret.peers.data_ptr(),
+                  off32[el:].data_ptr(), _stream())
         else:
+            self._exchange_done(_BWD_DISPATCH)
+            dw2 = K.group_xty(ctx.h, dyl, ol)
             dh = K.scatter2scatter(dyl, self.w2, ol, 1, GROUPED_TO_GROUPED, transpose_w=True, out=ctx.h,
                                    activation=ctx.activation, act_grad_of=ctx.h_pre)
         dw1 = K.group_xty(r, dh, ol)
@@ -329,6 +380,19 @@ class PeerExpertParallelSmoeMlp:
         if self.scaled:
             dp = self.dp_ret.view(torch.float32, (self.max_tokens * k,))[:n].reshape(t, k).clone()
         return PeerEpGradients(dx=dx, dw1=dw1, dw2=dw2, dp=dp)
+
+    def _dispatch(self, src: torch.Tensor, order: GroupedOrder, k: int, weights, dstart, dest: SymmetricBuffer,
+                  with_meta: bool, label: str, pw=None, arrive=None) -> None:
+        lib = _lib.load()
+        _call(label, lib.smoe_ep_dispatch_rows,
+              src.data_ptr(), src.shape[0], self.d, order.o.data_ptr(), order.bin_offsets.data_ptr(),
+              self.num_experts, k, None if weights is None else weights.data_ptr(), order.num_slots,
+              dstart.data_ptr(), self.e_local, self.world, dest.peers.data_ptr(),
+              self.recv_slot.peers.data_ptr() if with_meta else None,
+              self.recv_src.peers.data_ptr() if with_meta else None, self.rank,
+              pw.data_ptr() if (with_meta and self.scaled) else None,
+              self.recv_p.peers.data_ptr() if (with_meta and self.scaled) else None, self.cap,
+              None if arrive is None else arrive.data_ptr(), self.err.data_ptr(), _lib.SMOE_BF16, _stream())
 
     def _gemm_return(self, a: torch.Tensor, w: torch.Tensor, order_loc: GroupedOrder, transpose: bool,
                      dest: SymmetricBuffer, scratch: torch.Tensor | None = None) -> None:
@@ -344,14 +408,14 @@ class PeerExpertParallelSmoeMlp:
             return
         out = K.scatter2scatter(a, w, order_loc, 1, GROUPED_TO_GROUPED, transpose_w=transpose, out=scratch)
         _call("ep_return rows", lib.smoe_ep_return_rows, out.data_ptr(), n, self.d, slot, src,
-              dest.peers.data_ptr(), _lib.SMOE_BF16, _stream())
+              dest.peers.data_ptr(), order_loc.bin_offsets[self.e_local:].data_ptr(), _lib.SMOE_BF16, _stream())
 
-    def _recv_p(self, rows: int) -> torch.Tensor:
-        return self.recv_p.view(torch.float32, (self.cap,))[:rows]
+    def _recv_p(self) -> torch.Tensor:
+        return self.recv_p.view(torch.float32, (self.cap,))
 
     def _buffers(self):
         return (self.flags, self.counts, self.recv_x, self.recv_dy, self.recv_slot, self.recv_src, self.y_ret,
-                self.dx_ret, self.recv_p, self.dp_ret)
+                self.dx_ret, self.recv_p, self.dp_ret, self.arrive)
 
     def close(self) -> None:
         torch.cuda.synchronize()

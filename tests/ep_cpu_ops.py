@@ -23,38 +23,32 @@ class CpuOps:
                             validate=False)
 
     @staticmethod
-    def group(x, order_o32, fan_out, weights=None):
-        w = None if weights is None else _np(weights)
-        return torch.from_numpy(orc.group(_np(x), _np(order_o32).astype(np.int64), w, fan_out))
-
-    @staticmethod
-    def combine(p, y_hat):
-        return torch.from_numpy(orc.combine(_np(p), _np(y_hat)))
-
-    @staticmethod
-    def combine_grad_p(dy, y_hat, s, j):
-        return torch.from_numpy(orc.combine_grad_p(_np(dy), _np(y_hat), s, j))
+    def gather(x, rows_o32, fan_out):
+        return torch.from_numpy(orc.group(_np(x), _np(rows_o32).astype(np.int64), None, fan_out))
 
     @staticmethod
     def fanout_reduce(g, fan_out):
         return torch.from_numpy(orc.fanout_reduce(_np(g), fan_out))
 
     @staticmethod
-    def local_forward(r, w1, w2, o_loc, off_loc, activation):
-        o, off = _np(o_loc).astype(np.int64), _np(off_loc).astype(np.int64)
-        h_pre = orc.scatter2scatter(_np(r), _np(w1), o, off, 1, False, True)
-        h = orc.act(h_pre, activation)
-        y = orc.scatter2scatter(h, _np(w2), o, off, 1, True, False)
-        return torch.from_numpy(y), (o, off, h_pre, h)
+    def local_forward(r, p_recv, w1, w2, off_loc, activation, wait=None):
+        """The scaled expert MLP (p moved through layer 2), f64 accumulate, f32 storage."""
+        off = _np(off_loc).astype(np.int64)
+        o = np.arange(r.shape[0], dtype=np.int64)
+        h_pre = orc.scatter2scatter(_np(r), _np(w1), o, off, 1, True, True)
+        hp = (_np(p_recv).astype(np.float64)[:, None] * orc.act(h_pre, activation).astype(np.float64)).astype(np.float32)
+        y = orc.scatter2scatter(hp, _np(w2), o, off, 1, True, True)
+        return torch.from_numpy(y), (o, off, h_pre, hp)
 
     @staticmethod
-    def local_backward(r, w1, w2, saved, dy, activation):
-        o, off, h_pre, h = saved
-        gdy = orc.group(_np(dy), o)
-        dw2 = orc.group_xty(h, gdy, off)
-        dh = (orc.scatter2scatter(gdy, _np(w2), o, off, 1, True, True, transpose_w=True)
-              * orc.act_grad(h_pre, activation)).astype(np.float32)
-        xbar = orc.group(_np(r), o)
-        dw1 = orc.group_xty(xbar, dh, off)
-        dr = orc.scatter2scatter(dh, _np(w1), o, off, 1, True, False, transpose_w=True)
-        return torch.from_numpy(dr), torch.from_numpy(dw1), torch.from_numpy(dw2)
+    def local_backward(r, p_recv, w1, w2, saved, dy, activation):
+        o, off, h_pre, hp = saved
+        p = _np(p_recv).astype(np.float64)[:, None]
+        dyn = _np(dy)
+        dw2 = orc.group_xty(hp, dyn, off)
+        g = orc.scatter2scatter(dyn, _np(w2), o, off, 1, True, True, transpose_w=True).astype(np.float64)
+        dp = (g * orc.act(h_pre, activation).astype(np.float64)).sum(1).astype(np.float32)
+        dh = (p * g * orc.act_grad(h_pre, activation).astype(np.float64)).astype(np.float32)
+        dw1 = orc.group_xty(_np(r), dh, off)
+        dr = orc.scatter2scatter(dh, _np(w1), o, off, 1, True, True, transpose_w=True)
+        return torch.from_numpy(dr), torch.from_numpy(dw1), torch.from_numpy(dw2), torch.from_numpy(dp)

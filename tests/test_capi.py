@@ -21,7 +21,7 @@ def declared_functions():
 def test_library_exists_and_loads():
     assert _lib.LIB_PATH.exists(), "run python -m paper_2403_08245_b200.build"
     lib = _lib.load()
-    assert lib.smoe_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.smoe_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_every_declared_symbol_is_exported_and_bound():

@@ -2,7 +2,9 @@
 
 * CPU, world_size 2 (and 4), gloo backend: the count exchange, all-to-all-v
   dispatch / return, local grouped order and source-side un-permute + combine
-  reproduce the single-process oracle on the concatenated batch.
+  reproduce the single-process oracle on the concatenated batch (the EP path
+  runs the routing-weight-scaled MLP form: equal to the literal form up to
+  float32 rounding).
 * GPU (1 B200, NCCL world 1): the EP path through the CUDA ops is
   bit-identical to the single-GPU smoe_mlp_forward / backward.
 """
@@ -117,7 +119,7 @@ def test_ep_world1_nccl_bit_identical_to_single_gpu():
         w2 = ((torch.rand(e, de, d, device="cuda", generator=g) * 2 - 1) / 22).bfloat16()
         routing = sm.topk_select(torch.softmax(torch.randn(t, e, device="cuda", generator=g), 1), k)
         order = sm.compute_grouped_order(routing)
-        prev = sm.moe_layers.set_scaled(False)   # EP combines at the source, like the literal path
+        prev = sm.moe_layers.set_scaled(True)    # the NCCL EP path runs the routing-weight-scaled form
         try:
             y_ref, c = sm.smoe_mlp_forward(x, w1, w2, routing, order)
             gr = sm.smoe_mlp_backward(c, dy)

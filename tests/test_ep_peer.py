@@ -74,7 +74,7 @@ def _problem(world, shape):
     return x, dy, w1, w2, logits
 
 
-def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
+def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False, mode="eager"):
     os.environ["SMOE_EP_FUSED_RETURN"] = fused
     E, K, T_LOCAL = SHAPES[shape][:3]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -95,19 +95,60 @@ def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
         sl = slice(rank * T_LOCAL, (rank + 1) * T_LOCAL)
         el = E // world
         es = slice(rank * el, (rank + 1) * el)
+        cf = {"capacity_ok": 1.5, "capacity_overflow": 0.5}.get(mode)
         ep = PeerExpertParallelSmoeMlp(w1[es].contiguous(), w2[es].contiguous(), E, K, max_tokens=T_LOCAL,
-                                       timeout_s=120.0, scaled=scaled)
+                                       timeout_s=120.0, scaled=scaled, capacity_factor=cf)
         rt = sm.RoutingResult(routing.expert_idx[sl].contiguous(), routing.p[sl].contiguous(),
                               routing.gate_full[sl].contiguous(), renormalized=True, validate=False)
+        xs, dys = x[sl].contiguous(), dy[sl].contiguous()
+
+        def compare(y, gr):
+            return {"y": torch.equal(y, y_ref[sl]), "dx": torch.equal(gr.dx, g_ref.dx[sl]),
+                    "dp": torch.equal(gr.dp, g_ref.dp[sl]), "dw1": torch.equal(gr.dw1, g_ref.dw1[es]),
+                    "dw2": torch.equal(gr.dw2, g_ref.dw2[es])}
+
         ok = []
-        for it in range(2):      # twice: the second step reuses every buffer
-            y, ctx = ep.forward(x[sl].contiguous(), rt)
-            gr = ep.backward(ctx, dy[sl].contiguous())
+        if mode == "capacity_overflow":
+            y, ctx = ep.forward(xs, rt)
+            ep.backward(ctx, dys)
             torch.cuda.synchronize()
-            ep._check_err()
-            ok.append({"y": torch.equal(y, y_ref[sl]), "dx": torch.equal(gr.dx, g_ref.dx[sl]),
-                       "dp": torch.equal(gr.dp, g_ref.dp[sl]), "dw1": torch.equal(gr.dw1, g_ref.dw1[es]),
-                       "dw2": torch.equal(gr.dw2, g_ref.dw2[es])})
+            try:
+                ep.check()
+                raised = False
+            except RuntimeError as exc:
+                raised = "capacity" in str(exc)
+            dist.barrier()
+            ok.append({"overflow_reported": raised or rank != 0})
+        elif mode == "graph":
+            # one eager step (kernel attributes, allocator), then the whole EP
+            # fwd+bwd captured into a CUDA graph and replayed: the device-side
+            # epochs and layout make every replay a complete, synchronised step
+            y, ctx = ep.forward(xs, rt)
+            ep.backward(ctx, dys)
+            torch.cuda.synchronize()
+            dist.barrier()
+            graph = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(graph, stream=s):
+                    y_g, ctx_g = ep.forward(xs, rt)
+                    gr_g = ep.backward(ctx_g, dys)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for it in range(3):
+                graph.replay()
+                torch.cuda.synchronize()
+                ep.check()
+                ok.append(compare(y_g, gr_g))
+        else:
+            for it in range(2):      # twice: the second step reuses every buffer
+                y, ctx = ep.forward(xs, rt)
+                gr = ep.backward(ctx, dys)
+                torch.cuda.synchronize()
+                ep.check()
+                ok.append(compare(y, gr))
         ep.close()
         q.put((rank, ok, None))
     except Exception as exc:  # report instead of hanging the parent
@@ -125,10 +166,32 @@ def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False):
     (2, "1", "c4full", True)])
 def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape, scaled):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
+    _run_world(world, fused, shape, scaled, "eager")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,shape", [(2, "c1"), (4, "c4")])
+def test_peer_ep_step_replays_as_a_cuda_graph(world, shape):
+    """The whole EP fwd+bwd (count exchange, layout, gated expert GEMMs, fused
+    returns) has no host synchronisation: it captures into one CUDA graph per
+    rank and every replay is bit-identical to one GPU on the concatenated batch."""
+    _run_world(world, "1", shape, True, "graph")
+
+
+@pytest.mark.gpu
+def test_peer_ep_capacity_bound():
+    """capacity_factor=1.5 (1.5 T*k receive rows, not G*T*k) holds the skewed routing
+    bit-identically; the starved routing (every row to rank 0's experts) at 0.5
+    is reported by check() instead of writing past the buffers."""
+    _run_world(2, "1", "c1", True, "capacity_ok")
+    _run_world(2, "1", "starve", True, "capacity_overflow")
+
+
+def _run_world(world, fused, shape, scaled, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shape, scaled)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shape, scaled, mode)) for r in range(world)]
     for pr in procs:
         pr.start()
     results = {}
