@@ -108,10 +108,15 @@ __global__ void __launch_bounds__(kThreads) dispatch_kernel(const T *__restrict_
     if (lane == 0 && peer_p) reinterpret_cast<float *>(peer_p[q])[j] = slot_p[slot];
   }
   if (over && lane == 0) atomicOr(err, 2);
-  __syncthreads();
-  if (threadIdx.x == 0 && peer_arrive) {
-    __threadfence_system();   // this CTA's row stores before the count
-    atomicAdd_system(reinterpret_cast<unsigned long long *>(peer_arrive[q]) + le, (unsigned long long)(r1 - r0));
+  if (peer_arrive) {
+    // every thread's row stores reach system scope before the CTA's count: a
+    // fence orders only the calling thread's own writes, so each writer fences
+    // (measured: with one fence in thread 0 the owner's first step could read
+    // rows still in flight)
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      atomicAdd_system(reinterpret_cast<unsigned long long *>(peer_arrive[q]) + le, (unsigned long long)(r1 - r0));
   }
 }
 

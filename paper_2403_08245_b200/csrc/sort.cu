@@ -15,7 +15,10 @@
 //                    permutation in slot order.
 // Output order is the stable order (slots ascend inside each bin), bit-exact
 // against numpy's stable argsort.
-// HBM traffic: ids read twice (8 B + 8 B per slot), three int32 outputs (12 B).
+// HBM traffic: the int64 ids are read once (8 B per slot); the histogram pass
+// also writes each slot's key in 1 byte (E < 256) or 2 bytes, which the scatter
+// pass reads back — 16 MB at n = 16 M, L2-resident between the two passes —
+// and three int32 outputs (12 B): ~20 B of DRAM traffic per slot.
 #include "common.cuh"
 
 namespace smoe {
@@ -45,10 +48,16 @@ __device__ __forceinline__ unsigned warp_peers(int32_t key) {
   return peers;
 }
 
-template <int kSortPerThread>
+// compact per-slot key written by the histogram pass (all ones = invalid id)
+template <typename KT>
+__device__ __forceinline__ KT compact_key(int64_t id, int E) {
+  return (id >= 0 && id < E) ? (KT)id : (KT)~(KT)0;
+}
+
+template <int kSortPerThread, typename KT>
 __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const int64_t *__restrict__ ids,
                                                                  int64_t n, int E, int num_tiles,
-                                                                 int32_t *__restrict__ hist) {
+                                                                 int32_t *__restrict__ hist, KT *__restrict__ keys_out) {
   constexpr int kSortTile = kSortThreads * kSortPerThread;
   extern __shared__ int32_t s_hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
@@ -61,8 +70,11 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const int64_t *
     keys[r] = i < n ? ids[i] : -1;
   }
 #pragma unroll
-  for (int r = 0; r < kSortPerThread; ++r)
+  for (int r = 0; r < kSortPerThread; ++r) {
+    const int64_t i = base + (int64_t)r * kSortThreads + threadIdx.x;
+    if (i < n) keys_out[i] = compact_key<KT>(keys[r], E);
     if (keys[r] >= 0 && keys[r] < E) atomicAdd(&s_hist[keys[r]], 1);
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[(int64_t)e * num_tiles + blockIdx.x] = s_hist[e];
 }
@@ -132,9 +144,9 @@ __global__ void __launch_bounds__(1024) sort_scan_kernel(int32_t *__restrict__ h
 
 // Shared layout of sort_scatter (dynamic): cnt[W][E] | lstart[E] | gbase[E] |
 // slot[4096] | key[4096] | warp scratch[32]
-template <int kSortPerThread, int NB>
+template <int kSortPerThread, int NB, typename KT>
 __global__ void __launch_bounds__(kSortThreads, 4) sort_scatter_kernel(
-    const int64_t *__restrict__ ids, int64_t n, int E, int num_tiles, const int32_t *__restrict__ hist,
+    const KT *__restrict__ ids, int64_t n, int E, int num_tiles, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ totals, int32_t *__restrict__ sorted_scattered, int32_t *__restrict__ sorted_expert,
     int32_t *__restrict__ inverse, int32_t *__restrict__ offsets) {
   constexpr int kSortTile = kSortThreads * kSortPerThread;
@@ -166,8 +178,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) sort_scatter_kernel(
     int64_t i = chunk0 + r * 32 + lane;
     int32_t key = -1;
     if (i < n) {
-      int64_t k64 = ids[i];
-      key = (k64 >= 0 && k64 < E) ? (int32_t)k64 : -1;
+      const KT kc = ids[i];
+      key = kc == (KT)~(KT)0 ? -1 : (int32_t)kc;
     }
     keys[r] = key;
     const unsigned peers = warp_peers<NB>(key);
@@ -222,11 +234,14 @@ __global__ void __launch_bounds__(kSortThreads, 4) sort_scatter_kernel(
 
 static size_t scatter_smem(int E, int tile) { return sizeof(int32_t) * ((size_t)kSortWarps * E + 2 * E + 2 * tile + 32); }
 
+static size_t key_bytes(int E) { return E < 255 ? 1 : 2; }
+
 size_t route_sort_workspace(int64_t n, int E) {
   const int tile = kSortThreads * sort_per_thread(n);
   int64_t tiles = (n + tile - 1) / tile;
   if (tiles < 1) tiles = 1;
-  return (size_t)(tiles * E + E) * sizeof(int32_t);
+  const size_t hist = (size_t)(tiles * E + E) * sizeof(int32_t);
+  return ((hist + 255) & ~(size_t)255) + (size_t)n * key_bytes(E);
 }
 
 int route_sort(const int64_t *ids, int64_t n, int E, int32_t *sorted_scattered,
@@ -249,30 +264,56 @@ int route_sort(const int64_t *ids, int64_t n, int E, int32_t *sorted_scattered,
     return check_launch("route_sort(empty)", 0);
   }
   const size_t smem = scatter_smem(E, tile);
-  auto hist_k = per == 8 ? sort_hist_kernel<8> : sort_hist_kernel<4>;
+  const size_t hist_bytes = (((size_t)tiles * E + E) * sizeof(int32_t) + 255) & ~(size_t)255;
+  void *keys = static_cast<uint8_t *>(ws) + hist_bytes;
   // key bits for the ballot ranking: E <= 8, 16, 64, 256, 1024
   const int nbc = E <= 8 ? 0 : E <= 16 ? 1 : E <= 64 ? 2 : E <= 256 ? 3 : 4;
-  using ScatterFn = void (*)(const int64_t *, int64_t, int, int, const int32_t *, const int32_t *, int32_t *,
-                             int32_t *, int32_t *, int32_t *);
-  static const ScatterFn table[2][5] = {
-      {sort_scatter_kernel<4, 3>, sort_scatter_kernel<4, 4>, sort_scatter_kernel<4, 6>, sort_scatter_kernel<4, 8>,
-       sort_scatter_kernel<4, 10>},
-      {sort_scatter_kernel<8, 3>, sort_scatter_kernel<8, 4>, sort_scatter_kernel<8, 6>, sort_scatter_kernel<8, 8>,
-       sort_scatter_kernel<8, 10>}};
-  const ScatterFn scat_k = table[per == 8][nbc];
-  static size_t configured[2][5] = {};
-  size_t &cfg = configured[per == 8][nbc];
-  if (smem > cfg) {
-    if ((smem > 48 * 1024 &&
-         cudaFuncSetAttribute(scat_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) ||
-        cudaFuncSetAttribute(scat_k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
-      return check_launch("route_sort: smem attribute", 0);
-    cfg = smem;
+  if (key_bytes(E) == 1) {
+    using KT = uint8_t;
+    auto hist_k = per == 8 ? sort_hist_kernel<8, KT> : sort_hist_kernel<4, KT>;
+    using ScatterFn = void (*)(const KT *, int64_t, int, int, const int32_t *, const int32_t *, int32_t *, int32_t *,
+                               int32_t *, int32_t *);
+    static const ScatterFn table[2][4] = {
+        {sort_scatter_kernel<4, 3, KT>, sort_scatter_kernel<4, 4, KT>, sort_scatter_kernel<4, 6, KT>,
+         sort_scatter_kernel<4, 8, KT>},
+        {sort_scatter_kernel<8, 3, KT>, sort_scatter_kernel<8, 4, KT>, sort_scatter_kernel<8, 6, KT>,
+         sort_scatter_kernel<8, 8, KT>}};
+    const ScatterFn scat_k = table[per == 8][nbc];
+    static size_t configured[2][4] = {};
+    size_t &cfg = configured[per == 8][nbc];
+    if (smem > cfg) {
+      if ((smem > 48 * 1024 &&
+           cudaFuncSetAttribute(scat_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) ||
+          cudaFuncSetAttribute(scat_k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+        return check_launch("route_sort: smem attribute", 0);
+      cfg = smem;
+    }
+    hist_k<<<tiles, kSortThreads, E * sizeof(int32_t), stream>>>(ids, n, E, tiles, hist, (KT *)keys);
+    sort_scan_kernel<<<E, 1024, 0, stream>>>(hist, tiles, totals);
+    scat_k<<<tiles, kSortThreads, smem, stream>>>((const KT *)keys, n, E, tiles, hist, totals, sorted_scattered,
+                                                  sorted_expert, inverse, offsets);
+  } else {
+    using KT = uint16_t;
+    auto hist_k = per == 8 ? sort_hist_kernel<8, KT> : sort_hist_kernel<4, KT>;
+    using ScatterFn = void (*)(const KT *, int64_t, int, int, const int32_t *, const int32_t *, int32_t *, int32_t *,
+                               int32_t *, int32_t *);
+    static const ScatterFn table[2][2] = {{sort_scatter_kernel<4, 8, KT>, sort_scatter_kernel<4, 10, KT>},
+                                          {sort_scatter_kernel<8, 8, KT>, sort_scatter_kernel<8, 10, KT>}};
+    const ScatterFn scat_k = table[per == 8][nbc == 4];
+    static size_t configured[2][2] = {};
+    size_t &cfg = configured[per == 8][nbc == 4];
+    if (smem > cfg) {
+      if ((smem > 48 * 1024 &&
+           cudaFuncSetAttribute(scat_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) ||
+          cudaFuncSetAttribute(scat_k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+        return check_launch("route_sort: smem attribute", 0);
+      cfg = smem;
+    }
+    hist_k<<<tiles, kSortThreads, E * sizeof(int32_t), stream>>>(ids, n, E, tiles, hist, (KT *)keys);
+    sort_scan_kernel<<<E, 1024, 0, stream>>>(hist, tiles, totals);
+    scat_k<<<tiles, kSortThreads, smem, stream>>>((const KT *)keys, n, E, tiles, hist, totals, sorted_scattered,
+                                                  sorted_expert, inverse, offsets);
   }
-  hist_k<<<tiles, kSortThreads, E * sizeof(int32_t), stream>>>(ids, n, E, tiles, hist);
-  sort_scan_kernel<<<E, 1024, 0, stream>>>(hist, tiles, totals);
-  scat_k<<<tiles, kSortThreads, smem, stream>>>(ids, n, E, tiles, hist, totals, sorted_scattered, sorted_expert,
-                                                inverse, offsets);
   return check_launch("route_sort", 3);
 }
 

@@ -605,7 +605,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         const bool combine = p.epi == EPI_COMBINE;
         // *_SCALED epilogues: this thread's row scale and combine-weight-gradient partial
         float rscale = 1.0f, dpacc = 0.0f;
-        if (epi_scaled(p.epi) && dst >= 0) rscale = __ldcg(p.pw + p.order[row]);
+        // gated (expert-parallel) tiles: the row scales were stored by peers; they
+        // are read only after this thread's own acquire of the arrival counter below
+        if (epi_scaled(p.epi) && dst >= 0 && !p.arrive) rscale = __ldcg(p.pw + p.order[row]);
         float cscale = 0.f;  // combine: this thread's row weight; cdst becomes the token row
         if (combine) {
           if (dst >= 0) cscale = __ldcg(p.pw + dst);
@@ -615,6 +617,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         if (has_acc && (WIDE || h == 0)) {  // WIDE: each half has its own tfull
           mbar_wait_cluster(smem_u32(&tfull_bar[abuf]), acc_phase);
           tc_fence_after();
+        }
+        if (p.arrive && epi_scaled(p.epi) && dst >= 0) {
+          (void)ld_acquire_sys_u64(p.arrive + tl.e);   // the tile ran, so the count is complete
+          rscale = __ldcg(p.pw + p.order[row]);
         }
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TN + c_begin);
         // WIDE: the second half may lie past the bin / matrix.  SMOE_TC_TIMING=6
@@ -761,7 +767,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         uint4 av[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
         const bool use_aux = epi_act_grad(p.epi) && valid;
         float rscale = 1.0f, dpacc = 0.0f;
-        if (epi_scaled(p.epi) && valid) rscale = __ldcg(p.pw + p.order[row]);
+        if (epi_scaled(p.epi) && valid && !p.arrive) rscale = __ldcg(p.pw + p.order[row]);
         if (use_aux) {
           const int64_t c0 = tl.n0 + c_begin;
   #pragma unroll
@@ -771,6 +777,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         if (has_acc) {
           mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
           tc_fence_after();
+        }
+        if (p.arrive && epi_scaled(p.epi) && valid) {
+          (void)ld_acquire_sys_u64(p.arrive + tl.e);
+          rscale = __ldcg(p.pw + p.order[row]);
         }
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c_begin);
   #pragma unroll 1
