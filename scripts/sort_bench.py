@@ -9,6 +9,7 @@ scan -> scatter kernels), CUDA events, after warm-up.  One JSON line per n.
 """
 import ctypes
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -55,7 +56,7 @@ def main():
             ref = torch.sort(ids, stable=True).indices.to(torch.int32)
             assert torch.equal(ref, o), "sort mismatch"
         gbs = 20.0 * n / (us * 1e-6) / 1e9
-        print(json.dumps({"n": n, "E": e, "us": us, "algorithmic_bytes": 20 * n, "GBps": gbs,
+        print(json.dumps({"n": n, "E": e, "onepass_enabled": os.environ.get("SMOE_SORT_ONEPASS", "1") != "0", "us": us, "algorithmic_bytes": 20 * n, "GBps": gbs,
                           "frac_hbm": gbs / peaks["hbm_gbs"], "peak_hbm_gbs": peaks["hbm_gbs"]}), flush=True)
 
 

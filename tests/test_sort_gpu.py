@@ -44,7 +44,8 @@ def test_reference_property_cases():
 
 @pytest.mark.parametrize("t,k,e", [(4096, 2, 8), (32768, 2, 8), (32768, 8, 64), (32768, 4, 16),
                                    (5000, 3, 7), (1, 1, 1), (4097, 1, 1), (70000, 2, 1024),
-                                   (300001, 4, 1024), (600000, 2, 5), (262145, 4, 2)])
+                                   (300001, 4, 1024), (600000, 2, 5), (262145, 4, 2),
+                                   (70001, 3, 256), (50001, 1, 255), (1 << 20, 2, 8), (12289, 1, 3)])
 def test_baseline_sizes_random(t, k, e):
     rng = np.random.default_rng(t + k + e)
     idx = np.stack([rng.permutation(e)[:k] for _ in range(min(t, 2000))])
@@ -75,3 +76,20 @@ def test_flatten_and_sort_api():
     assert ss.tolist() == [0, 3, 2, 1]
     assert se.tolist() == [0, 0, 1, 2]
     assert offs.tolist() == [2, 3, 4]
+
+
+def test_two_pass_path_same_suite():
+    """The same cases through the two-pass kernels (SMOE_SORT_ONEPASS=0): the
+    one-pass cooperative kernel is the default whenever a chunk fits in shared
+    memory, the two-pass path serves larger n and E > 256."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    if os.environ.get("SMOE_SORT_ONEPASS") == "0":
+        pytest.skip("already the two-pass run")
+    here = Path(__file__).resolve()
+    env = dict(os.environ, SMOE_SORT_ONEPASS="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", str(here), "-m", "gpu",
+                        "-k", "not two_pass"], cwd=here.parent.parent, env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
