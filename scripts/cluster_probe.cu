@@ -1,0 +1,26 @@
+// How many thread-block clusters of size 2/4/8 (one CTA per SM, ~225 KB smem)
+// can be co-resident on this GPU: the SM cost of larger multicast clusters.
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void k(int *p) { if (p) p[blockIdx.x] = 1; }
+int main() {
+  int smem = 225 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  int dev = 0, sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int cs : {1, 2, 4, 6, 8, 16}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 64);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = cs; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
+    cfg.attrs = a; cfg.numAttrs = 1;
+    int n = -1;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
+    printf("cluster %2d: max active clusters %d -> %d SMs of %d (%s)\n", cs, n, n * cs, sms, cudaGetErrorString(e));
+  }
+  return 0;
+}
