@@ -228,6 +228,20 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
     uint32_t phase = 0;
     // the leader claims one tile ahead, so the atomic's latency hides behind a tile's loads
     int64_t t_next = leader ? claim_tile(0) : 0;
+    // wave lockstep (leader only): chunks issued so far, and the last seen
+    // minimum over all clusters (refreshed only when it no longer admits us)
+    const bool lockstep = leader && p.sync_chunk > 0;
+    uint32_t v_mine = 0, v_min = 0;
+    auto lockstep_gate = [&]() {
+      ++v_mine;
+      if (lane == 0) st_relaxed_gpu_u32(p.prog + cluster_id, v_mine);
+      while (v_mine > v_min + (uint32_t)p.sync_slack) {
+        uint32_t m = 0xffffffffu;
+        for (int c = lane; c < p.nclusters; c += 32) m = min(m, ld_relaxed_gpu_u32(p.prog + c));
+        v_min = __reduce_min_sync(0xffffffffu, m);
+        if (v_mine > v_min + (uint32_t)p.sync_slack) __nanosleep(256);
+      }
+    };
     for (int it = 0;; ++it) {
       int64_t t;
       if (leader) {
@@ -236,7 +250,16 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       } else {
         t = next_tile(it);
       }
-      if (t < 0) break;
+      if (t < 0) {
+        // out of tiles: never gate the others again
+        if (lockstep && lane == 0) st_relaxed_gpu_u32(p.prog + cluster_id, 0xffffffffu);
+        break;
+      }
+      if (p.timing == 7 && leader && lane == 0 && it < 16) {  // debug: tile start times (wave drift)
+        uint64_t gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        printf("tiletrace %d %lld %llu\n", (int)cluster_id, (long long)t, (unsigned long long)gt);
+      }
       const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
       const int m_half = (int)(tl.m0 + HM * rank);  // A rows / B columns of this CTA
       const int n_half = (int)(tl.n0 + HN * rank);
@@ -261,6 +284,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         const int kk = kb * BK;
         // all lanes wait (keeps the warp converged, so coordinates and
         // addresses stay in uniform registers); one elected lane issues
+        if (lockstep && kb % p.sync_chunk == 0) lockstep_gate();
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         if (elect_one_sync()) {
           const uint32_t sb = sa + ABYTES;
@@ -1010,15 +1034,45 @@ namespace tc2 {
 // Tile counters of the dynamic schedule: one zeroed (stream-ordered memset) per
 // launch; a 64-entry pool so launches in flight on different streams never
 // share one.
-__device__ uint32_t g_tile_ctr[64];
+// Each entry: [0] the tile counter, [1, 1 + 128) the clusters' lockstep
+// progress; both zeroed by one memset per launch.
+constexpr int kSyncSlots = 128;
+__device__ uint32_t g_tile_ctr[64][1 + kSyncSlots];
 
-static uint32_t *tile_counter(cudaStream_t st) {
+static uint32_t *tile_counter(cudaStream_t st, bool with_prog) {
   static uint32_t *base = nullptr;
   static std::atomic<unsigned> seq{0};
   if (!base && cudaGetSymbolAddress((void **)&base, g_tile_ctr) != cudaSuccess) return nullptr;
-  uint32_t *c = base + (seq.fetch_add(1) % 64);
-  if (cudaMemsetAsync(c, 0, sizeof(uint32_t), st) != cudaSuccess) return nullptr;
+  uint32_t *c = base + (seq.fetch_add(1) % 64) * (1 + kSyncSlots);
+  if (cudaMemsetAsync(c, 0, sizeof(uint32_t) * (with_prog ? 1 + kSyncSlots : 1), st) != cudaSuccess) return nullptr;
   return c;
+}
+
+// Wave lockstep of the long-K GEMMs.  With the in-order dynamic schedule the
+// pairs running at once hold neighbouring tiles whose operand panels (up to
+// 512 rows x K) they share — but only while they stream K in step: measured at
+// C1 layer 2, the start times within a 74-tile wave spread to a whole tile
+// duration (p10-p90 ~200 us of 222) after four waves, tile times vary
+// 185-277 us, and each tile re-reads its panels from DRAM (9.5 GB against
+// 3.4 GB algorithmic; profiles/r2_lockstep.txt).  Each leader therefore issues
+// its ring chunk v (sync_chunk k-blocks) only while v <= min over clusters of
+// the chunks issued + sync_slack, so concurrent tiles stay within slack chunks
+// of each other and a panel slice is fetched from DRAM about once per wave.
+// The slowest cluster never waits, so the gate cannot deadlock while all
+// clusters are resident (the grid is sized to the resident pairs); clusters
+// out of tiles publish UINT_MAX.  Off for the expert-parallel gated kernels.
+// SMOE_TC_SYNC = k-blocks per chunk (0 = off), SMOE_TC_SYNC_SLACK = chunks.
+static void set_lockstep(Params &q, int clusters, bool eligible) {
+  static int chunk = -1, slack = -1;
+  if (chunk < 0) {
+    const char *env = getenv("SMOE_TC_SYNC");
+    chunk = env ? atoi(env) : 0;
+    env = getenv("SMOE_TC_SYNC_SLACK");
+    slack = env ? atoi(env) : 8;
+  }
+  q.sync_chunk = (eligible && chunk > 0 && !q.arrive && clusters <= kSyncSlots) ? chunk : 0;
+  q.sync_slack = slack;
+  q.nclusters = clusters;
 }
 
 // L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: off (default) |
@@ -1062,8 +1116,12 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   if (max_tiles < clusters) clusters = (int)(max_tiles > 0 ? max_tiles : 1);
   Params q = p;
   set_l2_policy(q, clusters, TN);
-  q.tile_ctr = tile_counter(st);
+  // the wide (long-K, TMA-fed) kernels only: gating the gather kernels' ring
+  // starves their cp.async warps (C1 layer 1: 5.6 -> 6.7 ms under ncu)
+  set_lockstep(q, clusters, WIDE && !has_gather(AM, BMODE));
+  q.tile_ctr = tile_counter(st, q.sync_chunk > 0);
   if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
+  q.prog = q.tile_ctr + 1;
   kern<<<2 * clusters, kernel_threads(AM, BMODE), smem, st>>>(ta, tb, tc, tc2, q);
   return check_launch("tc2_gemm");
 }

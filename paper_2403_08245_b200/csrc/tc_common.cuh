@@ -54,8 +54,23 @@ struct Params {
   // loading a tile of local expert e the producer waits until arrive[e] (a
   // peer-incremented row counter) reaches the expert's bin length.
   const unsigned long long *arrive;
+  // K-lockstep of the cluster pairs (see tc2_gemm.cu, "wave lockstep"): each
+  // leader publishes the ring chunks it has issued in prog[cluster] and issues
+  // chunk v only while v <= min over clusters + sync_slack.  0 = off.
+  uint32_t *prog;
+  int sync_chunk;   // k-blocks per chunk
+  int sync_slack;   // chunks
+  int nclusters;
 };
 
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
