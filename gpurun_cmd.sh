@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests/test_sort_gpu.py -q -p no:cacheprovider -x 2>&1 | tail -3
-SMOE_SORT_MATCH=1 timeout 600 python -m pytest tests/test_sort_gpu.py -q -p no:cacheprovider -x -k "not two_pass" 2>&1 | tail -3
-timeout 300 python scripts/sort_bench.py 65536:8 262144:64 1048576:8 16777216:64 16777216:8 16777216:256 2>&1 | tail -6
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/gpu_full_s3.log 2>&1; tail -5 gpurun_out/gpu_full_s3.log
+timeout 600 python bench.py > gpurun_out/bench_c1_s3.json 2> gpurun_out/bench_c1_s3.err; tail -c 400 gpurun_out/bench_c1_s3.json
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
