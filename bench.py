@@ -260,19 +260,20 @@ def run_ours(args, rank, world, local_rank):
             from paper_2403_08245_b200.ep import ExpertParallelSmoeMlp
             ep = ExpertParallelSmoeMlp(w1, w2, E)
 
-        def step(xx, dyy, rt, dy_ready=None):
+        def step(xx, dyy, rt, dy_ready=None, on_dx=None):
             y, ctx = ep.forward(xx, rt)
             if dy_ready is not None:
                 dy_ready()
             grads = ep.backward(ctx, dyy)
             return y, grads
     else:
-        def step(xx, dyy, rt, dy_ready=None):
+        def step(xx, dyy, rt, dy_ready=None, on_dx=None):
             order = sm.compute_grouped_order(rt)
             y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
             if dy_ready is not None:   # e2e: dY's H2D copy overlaps the forward
                 dy_ready()
-            grads = sm.smoe_mlp_backward(ctx, dyy)
+            # e2e: dX / dp leave while dW1 computes (the public API's on_dx hook)
+            grads = sm.smoe_mlp_backward(ctx, dyy, on_dx=on_dx)
             return y, grads
 
     def barrier():
@@ -376,14 +377,24 @@ def run_ours(args, rank, world, local_rank):
             b = dbufs[slot]
             rt = sm.RoutingResult(expert_idx=b["ids"], p=b["p"], gate_full=routing.gate_full, renormalized=True,
                                   validate=False)
-            _, grads = step(b["x"], b["dy"], rt, dy_ready=lambda: st.wait_event(ev_dy[slot]))
+            sent = []
+
+            def send_results(dx_, dp_):
+                # D2H of this step's results as soon as they are enqueued
+                ev_res = torch.cuda.Event()
+                ev_res.record(st)
+                with torch.cuda.stream(cs_out):
+                    cs_out.wait_event(ev_res)
+                    hdx.copy_(dx_, non_blocking=True)
+                    hdp.copy_(dp_, non_blocking=True)
+                    dx_.record_stream(cs_out)
+                    dp_.record_stream(cs_out)
+                sent.append(True)
+
+            _, grads = step(b["x"], b["dy"], rt, dy_ready=lambda: st.wait_event(ev_dy[slot]), on_dx=send_results)
             ev_done[slot].record(st)
-            with torch.cuda.stream(cs_out):
-                cs_out.wait_event(ev_done[slot])
-                hdx.copy_(grads.dx, non_blocking=True)
-                hdp.copy_(grads.dp, non_blocking=True)
-                grads.dx.record_stream(cs_out)
-                grads.dp.record_stream(cs_out)
+            if not sent:   # paths without the hook (expert-parallel): after the step
+                send_results(grads.dx, grads.dp)
         st.wait_stream(cs)
         st.wait_stream(cs_out)
 

@@ -223,16 +223,21 @@ def smoe_mlp_forward(
 
 
 def smoe_mlp_backward(ctx: SmoeMlpContext, dy: torch.Tensor, *, tile: TileConfig | None = None,
-                      ledger=None) -> SmoeMlpGradients:
+                      ledger=None, on_dx=None) -> SmoeMlpGradients:
     """Gradients for the routed MLP; stops at dp (moe_layers.py:185-211).
 
     Reuse: the output transform's input gradients land in the activated hidden
     buffer (after dW2 consumed it) with act'(h_pre) fused in; the retained
     pre-combine output's storage takes the hidden transform's grouped input.
     No new T*k-row buffer is allocated.
+
+    on_dx(dx, dp): optional hook, called as soon as the kernels producing dX
+    and dp are enqueued on the current stream (the bf16 path enqueues the
+    input gradient before the last weight gradient), so a caller can start
+    dX's copy or communication while dW1 computes.
     """
     if ctx.scaled is not None:
-        return _scaled_backward(ctx, dy)
+        return _scaled_backward(ctx, dy, on_dx)
     out_ctx = ctx.output_ctx
     hid_ctx = ctx.hidden_ctx
     out_ctx.scratch_grouped_x = out_ctx.x
@@ -241,14 +246,18 @@ def smoe_mlp_backward(ctx: SmoeMlpContext, dy: torch.Tensor, *, tile: TileConfig
     dh = g2.dx
     hid_ctx.scratch_grouped_x = out_ctx.y_hat
     g1 = pl.backward(hid_ctx, dh, tile=tile, ledger=ledger, name="mlp.hidden")
+    if on_dx is not None:
+        on_dx(g1.dx, g2.dp)
     return SmoeMlpGradients(dx=g1.dx, dw1=g1.dw, dw2=g2.dw, dp=g2.dp)
 
 
-def _scaled_backward(ctx: SmoeMlpContext, dy: torch.Tensor) -> SmoeMlpGradients:
-    """Backward of the routing-weight-scaled path; same buffer reuse as the
-    reference (moe_layers.py:198-211): grouped dY and then the grouped input
-    live in the retained output's storage, dH overwrites p * act(h_pre) after
-    dW2 consumed it, the slot input-gradients overwrite the grouped input."""
+def _scaled_backward(ctx: SmoeMlpContext, dy: torch.Tensor, on_dx=None) -> SmoeMlpGradients:
+    """Backward of the routing-weight-scaled path; the reference's buffer reuse
+    (moe_layers.py:198-211): grouped dY lives in the retained output's
+    storage, dH overwrites p * act(h_pre) after dW2 consumed it.  The input
+    gradient is produced before dW1 (dX is what the upstream layer waits for):
+    the slot input-gradients take grouped dY's storage, and after their k-sum
+    the grouped input for dW1 reuses it — still no new T*k-row buffer."""
     st = ctx.scaled
     order, k = st.order, st.p.shape[1]
     t = st.p.shape[0]
@@ -264,15 +273,16 @@ def _scaled_backward(ctx: SmoeMlpContext, dy: torch.Tensor) -> SmoeMlpGradients:
                                   activation=ctx.activation, out=st.hp, act_grad_of=ctx.h_pre,
                                   dp_partials=parts, transpose_w=True)
     dp = K.dp_from_partials(parts, order, t, k)
+    slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_SCATTERED, transpose_w=True, out=dyg)
+    dx = K.fanout_reduce(slot, k)
+    if on_dx is not None:
+        on_dx(dx, dp)
     if pl._gather_ok(de, st.x) and order.num_experts <= 128:
         dw1 = K.group_xty_scattered(st.x, dh, order, x_fan_out=k, y_grouped=True)
-        slot_out = dyg
     else:
+        # stream order: the k-sum above has read the slot gradients first
         xbar = K.group(st.x, order, fan_out=k, out=dyg)
         dw1 = K.group_xty(xbar, dh, order)
-        slot_out = xbar
-    slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_SCATTERED, transpose_w=True, out=slot_out)
-    dx = K.fanout_reduce(slot, k)
     return SmoeMlpGradients(dx=dx, dw1=dw1, dw2=dw2, dp=dp)
 
 

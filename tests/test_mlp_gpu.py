@@ -342,3 +342,26 @@ def test_zero_tokens(training):
         torch.cuda.synchronize()
         assert tuple(gr.dx.shape) == (0, d) and tuple(gr.dp.shape) == (0, k)
         assert float(gr.dw1.abs().max()) == 0.0 and float(gr.dw2.abs().max()) == 0.0
+
+
+def test_on_dx_hook_fires_before_dw1_with_final_dx():
+    """smoe_mlp_backward(on_dx=...) hands over dX and dp as soon as their kernels
+    are enqueued; the tensors are the returned gradients (bit-identical values)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    tokens, d, de, e, k = 1024, 256, 512, 8, 2
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / de ** 0.5).to(torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+    order = sm.compute_grouped_order(routing)
+    seen = []
+    y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+    gr = sm.smoe_mlp_backward(ctx, dy, on_dx=lambda dx, dp: seen.append((dx.clone(), dp.clone())))
+    assert len(seen) == 1
+    torch.cuda.synchronize()
+    assert torch.equal(seen[0][0], gr.dx) and torch.equal(seen[0][1], gr.dp)
+    y2, ctx2 = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+    gr2 = sm.smoe_mlp_backward(ctx2, dy)
+    for a, b in ((gr.dx, gr2.dx), (gr.dw1, gr2.dw1), (gr.dw2, gr2.dw2), (gr.dp, gr2.dp)):
+        assert torch.equal(a, b)
