@@ -400,6 +400,22 @@ __device__ __forceinline__ void zero_k_tail(uint8_t *base, int boxes, int valid,
   zero_k_rows(base, boxes, valid, 64, lane);
 }
 
+// SMOE_STORE_EVICT_FIRST (build-time A/B): epilogue output stores carry an
+// L2 evict-first policy, so the GEMM's streaming outputs do not push its
+// re-read operand panels out of L2.
+#ifndef SMOE_STORE_EVICT_FIRST
+#define SMOE_STORE_EVICT_FIRST 0
+#endif
+__device__ __forceinline__ void st_out128(void *p, uint4 v) {
+#if SMOE_STORE_EVICT_FIRST
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(0x12F0000000000000ull)
+               : "memory");
+#else
+  *reinterpret_cast<uint4 *>(p) = v;
+#endif
+}
+
 // Epilogue for one 16-column chunk of one accumulator row (fp32 in v[]);
 // scale / dpacc serve the *_SCALED epilogues (see epilogue_pack32).
 __device__ __forceinline__ void epilogue_chunk(const Params &p, const uint32_t (&v)[16], const uint4 (&av)[2],
@@ -450,9 +466,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params &p, const uint32_t (
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     if (col0 + 8 * j >= p.N) break;
-    *reinterpret_cast<uint4 *>(orow + col0 + 8 * j) = make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+    st_out128(orow + col0 + 8 * j, make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]));
     if (p.epi == SMOE_EPI_ACT || p.epi == SMOE_EPI_ACT_SCALED)
-      *reinterpret_cast<uint4 *>(orow2 + col0 + 8 * j) = make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
+      st_out128(orow2 + col0 + 8 * j, make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]));
   }
 }
 
@@ -570,9 +586,15 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 // TMA tile store smem -> global (bulk-group completion), SWIZZLE_128B maps.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int c0, int c1) {
+#if SMOE_STORE_EVICT_FIRST
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"((uint64_t)map),
+               "r"(src), "r"(c0), "r"(c1), "l"(0x12F0000000000000ull)
+               : "memory");
+#else
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
                "r"(src), "r"(c0), "r"(c1)
                : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // the smem source of every committed store has been read (buffer reusable)
@@ -638,7 +660,7 @@ __device__ __forceinline__ void store_staged_rows(uint32_t stg, __nv_bfloat16 *b
     const uint4 val = lds128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4));
     if (cdst[i] >= 0 && col_ok) {
       __nv_bfloat16 *rowp = base ? base + cdst[i] * ld : reinterpret_cast<__nv_bfloat16 *>(cdst[i]);
-      *reinterpret_cast<uint4 *>(rowp + col0 + cc * 8) = val;
+      st_out128(rowp + col0 + cc * 8, val);
     }
   }
   __syncwarp();
