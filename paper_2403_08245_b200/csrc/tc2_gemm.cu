@@ -494,7 +494,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
-              if (!(GA && GB) && valid < 16 * nk) zero_k_rows(sa_ptr, 4, valid, 16 * nk, lane);
+              // TMA-fed operands only (a gathered operand's copies zero-fill past the bin)
+              if (!(GA && GB) && valid < 16 * nk)
+                zero_k_rows(sa_ptr + ((KGATHER && GA) ? A_BYTES : 0), KGATHER ? 2 : 4, valid, 16 * nk, lane);
             }
           }
           if (RELAY) fence_proxy_async_smem();
@@ -568,7 +570,10 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             // the next expert; zero them up to the K16 step the leader issues
             const int valid = (int)(tl.k_len - (int64_t)kb * BK);
             const int upto = 16 * ((valid + 15) / 16);
-            if (valid < BK && valid < upto) zero_k_rows(tiles_smem + stage * SBYTES, 4, valid, upto, lane);
+            // only the TMA-fed operand's two boxes: the gathered one's rows past
+            // the bin were zero-filled by its copies (src-size 0)
+            if (valid < BK && valid < upto)
+              zero_k_rows(tiles_smem + stage * SBYTES + (GA ? A_BYTES : 0), 2, valid, upto, lane);
           }
           fence_proxy_async_smem();
           __syncwarp();
