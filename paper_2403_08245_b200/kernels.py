@@ -287,13 +287,15 @@ def scatter_combine(
     x, w = _cuda(x, "x"), _cuda(w, "w")
     p32 = _cuda(p_flat.to(_wdtype(x)), "p_flat")
     rows = num_slots // combine_cols
-    if (x.dtype == torch.bfloat16 and combine_cols > 2 and _COMBINE_FUSED != "1"
+    if (x.dtype == torch.bfloat16 and _COMBINE_FUSED != "1"
             and (engine or _engine) != "simt") or _COMBINE_FUSED == "0":
-        # k > 2: the fused epilogue's k fp32 additions per token land in completion
-        # order (not bit-reproducible) and its L2 reductions cost more than a
-        # scattered-output GEMM + the token-major combine (C2 layer 2: 4.13 vs
-        # 3.06 + 0.48 ms), so take that route; the n-row buffer it needs is the
-        # memory the fused form saves.
+        # bf16: a scattered-output GEMM + the token-major combine.  The fused
+        # combine epilogue (SMOE_COMBINE_FUSED=1) issues n*d_out fp32 L2
+        # reductions, which cost more than the n-row round trip (C1 inference:
+        # 11.15-11.36 vs 11.34-11.62 ms per forward; C2 layer 2: 3.06 + 0.48 vs
+        # 4.13 ms), its fp32 accumulator is as large as the n-row buffer at
+        # k = 2 (T*d*4 = T*k*d*2 B), and for k > 2 its additions land in
+        # completion order (not bit-reproducible).
         y_hat = scatter2scatter(x, w, order, fan_out, LayoutFlag(grouped_in, False), engine=engine)
         return combine(p32.view(rows, combine_cols), y_hat)
     acc = torch.empty((rows, d_out), dtype=_wdtype(x), device=x.device)

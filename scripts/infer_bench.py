@@ -2,8 +2,9 @@
 
 The inference path is the reference's scatter_combine route (kernels.py:242-286,
 parallel_linear.py:120-126): layer 1 S->G with the activation fused (no
-pre-activation kept), layer 2 as scatter_combine (p-scaled rows reduced into
-the token rows in the GEMM epilogue; no T*k output buffer).  FLOPs per forward
+pre-activation kept), layer 2 as scatter_combine (bf16: a scattered-output
+GEMM + the token-major combine; SMOE_COMBINE_FUSED=1 reduces the p-scaled
+rows into fp32 token rows in the GEMM epilogue instead).  FLOPs per forward
 = 4*T*k*d*d_e.  Prints one JSON line with per-kernel times (launch_timer).
 usage: python scripts/infer_bench.py [C1|C2] [engine]
 """

@@ -194,19 +194,25 @@ def test_scatter_combine_bf16_tcgen05(grouped_in, flavor):
         ys = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
                                 t(p.reshape(-1)), k, grouped_in, engine="simt")
         assert rel_err(y, np_of(ys)) <= 1e-2
-        # k <= 2: two fp32 additions into a zeroed row commute; k > 2 runs GEMM + combine
+        # default (GEMM to slot rows + token-major combine): deterministic
         y2 = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
                                 t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
         assert torch.equal(y, y2)
-        if k > 2:  # the fused epilogue forced at k > 2 (reductions in completion order)
-            prev = sm.kernels._COMBINE_FUSED
-            sm.kernels._COMBINE_FUSED = "1"
-            try:
-                yf = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
-                                        t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
-            finally:
-                sm.kernels._COMBINE_FUSED = prev
-            assert rel_err(yf, want) <= 2e-2
+        # the fused combine epilogue (SMOE_COMBINE_FUSED=1): p-scaled rows reduced
+        # into fp32 token rows in L2; k <= 2 is bit-reproducible (two additions
+        # into a zeroed row commute), k > 2 lands in completion order
+        prev = sm.kernels._COMBINE_FUSED
+        sm.kernels._COMBINE_FUSED = "1"
+        try:
+            yf = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                    t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+            yf2 = sm.scatter_combine(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out,
+                                     t(p.reshape(-1)), k, grouped_in, engine="tcgen05")
+        finally:
+            sm.kernels._COMBINE_FUSED = prev
+        assert rel_err(yf, want) <= 2e-2
+        if k <= 2:
+            assert torch.equal(yf, yf2)
 
 
 def test_inference_mlp_uses_tcgen05_combine():
@@ -223,9 +229,18 @@ def test_inference_mlp_uses_tcgen05_combine():
     with LaunchTimer() as lt:
         y_inf, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=False)
     labels = list(lt.summary())
-    assert any(lab.startswith("scatter_combine") for lab in labels), labels
+    assert any(lab.startswith("scatter2scatter G->S") for lab in labels), labels
     y_tr, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=True)
     assert rel_err(y_inf, np_of(y_tr)) <= 1e-2
+    prev = sm.kernels._COMBINE_FUSED
+    sm.kernels._COMBINE_FUSED = "1"
+    try:
+        with LaunchTimer() as lt:
+            y_fused, _ = sm.smoe_mlp_forward(x, w1, w2, routing, order, training=False)
+    finally:
+        sm.kernels._COMBINE_FUSED = prev
+    assert any(lab.startswith("scatter_combine") for lab in lt.summary())
+    assert rel_err(y_fused, np_of(y_tr)) <= 1e-2
 
 
 @pytest.mark.parametrize("engine", ["auto", "simt"])

@@ -167,8 +167,11 @@ for (t, k, e, d, de) in ((2100, 2, 8, 264, 584), (700, 3, 16, 136, 1032), (37, 1
                                                   activation='gelu', out=torch.empty_like(h), act_out=a.clone()))
     outs.append(sm.group_xty(xg, h, o, engine='tcgen05'))
     outs.append(sm.group_xty(h, xg, o, engine='tcgen05'))
+    outs.append(sm.scatter_combine(h, wt, o, 1, p.reshape(-1).contiguous(), k, True, engine='tcgen05'))
     if k <= 2:   # fused combine epilogue: two fp32 additions into a zeroed row commute
+        sm.kernels._COMBINE_FUSED = '1'
         outs.append(sm.scatter_combine(h, wt, o, 1, p.reshape(-1).contiguous(), k, True, engine='tcgen05'))
+        sm.kernels._COMBINE_FUSED = 'auto'
 torch.save([x.cpu() for x in outs], sys.argv[1])
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     runs = {}
