@@ -163,7 +163,7 @@ def _worker(rank, world, port, q, fused="1", shape="c1", scaled=False, mode="eag
 @pytest.mark.parametrize("world,fused,shape,scaled", [
     (2, "1", "c1", False), (4, "1", "c1", False), (2, "0", "c1", False), (4, "1", "c4", False),
     (2, "1", "starve", False), (2, "1", "c1", True), (4, "1", "c4", True), (2, "1", "starve", True),
-    (2, "1", "c4full", True)])
+    (2, "1", "c4full", True), (8, "1", "c4", True)])
 def test_peer_ep_processes_sharing_one_gpu_bit_identical(world, fused, shape, scaled):
     """fused = the return stored by the expert GEMM's epilogue; 0 = GEMM + return kernel."""
     _run_world(world, fused, shape, scaled, "eager")
