@@ -1,3 +1,4 @@
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -o scripts/_bin/cluster_probe scripts/cluster_probe.cu
 // How many thread-block clusters of size 2/4/8 (one CTA per SM, ~225 KB smem)
 // can be co-resident on this GPU: the SM cost of larger multicast clusters.
 #include <cstdio>
