@@ -85,6 +85,18 @@ __host__ __device__ constexpr int kernel_threads(int am, int bm) {
   return 64 + 32 * EPI_WARPS + 32 * gather_warps(am, bm);
 }
 
+// The epilogue warps wait for an accumulator through one of them: warp 0 polls
+// the tile-full mbarrier, the others block on a named barrier (no issue slots
+// while blocked).  A suspended mbarrier try_wait is woken by every barrier
+// event of the CTA (a ring stage or an empty slot every few hundred cycles),
+// so eight polling warps re-issued their wait loop ~300 M times per C1 GEMM
+// launch (ncu smsp__inst_executed, 256 x 256 tiles: 420 M of which ~100 M are
+// work) regardless of the suspend hint.
+__device__ __forceinline__ void epi_wait_full(uint32_t bar, uint32_t parity, int epi_warp) {
+  if (epi_warp == 0) mbar_wait_cluster(bar, parity);
+  asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+}
+
 template <int AM, int BMODE, bool GK, bool STAGED, bool WIDE>
 __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__(2, 1, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           for (int i = 0; i < 8; ++i) cdst[i] = cdst[i] >= 0 ? cdst[i] / p.combine_cols : -1;
         }
         if (has_acc && (WIDE || h == 0)) {  // WIDE: each half has its own tfull
-          mbar_wait_cluster(smem_u32(&tfull_bar[abuf]), acc_phase);
+          epi_wait_full(smem_u32(&tfull_bar[abuf]), acc_phase, warp);
           tc_fence_after();
         }
         if (p.arrive && epi_scaled(p.epi) && dst >= 0) {
@@ -804,7 +816,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             if (c0 + 8 * j < p.N) av[j] = __ldg(reinterpret_cast<const uint4 *>(arow + c0 + 8 * j));
         }
         if (has_acc) {
-          mbar_wait_cluster(smem_u32(&tfull_bar[acc]), acc_phase);
+          epi_wait_full(smem_u32(&tfull_bar[acc]), acc_phase, ew);
           tc_fence_after();
         }
         if (p.arrive && epi_scaled(p.epi) && valid) {

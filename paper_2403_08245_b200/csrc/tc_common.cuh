@@ -103,12 +103,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// mbarrier waits carry a suspend-time hint: a waiting warp is parked until the
-// phase completes (or the hint, in ns, expires and the loop re-tries) instead
-// of re-issuing try_wait.  Without it the epilogue warps, waiting out a whole
-// tile's mainloop, were 65 % of a GEMM's executed warp instructions
-// (profiles/r1_wide_tiles.txt) — issue energy the 1 kW power cap takes out of
-// the clock.  SMOE_WAIT_HINT=0 builds the hint-free spin (A/B).
+// mbarrier waits use try_wait (a potentially blocking wait: the warp is parked
+// until the phase completes, a barrier event in the CTA wakes it, or the
+// suspend-time hint expires) rather than a test_wait busy loop.  Measured
+// (round 2, scripts/_bin variants): the explicit hint changes nothing against
+// try_wait's default limit — C1 256x256 GEMM 417.7 vs 418.6 M executed warp
+// instructions, dW 261.7 vs 260.5 M, step within noise — and the wait loops
+// are ~12 % of the 256x256 kernel's instructions (ncu source counters: TMA
+// producer ~25 %, MMA issue loop ~29 %, epilogue ~34 %).  SMOE_WAIT_HINT=0
+// builds the hint-free form (A/B).
 #ifndef SMOE_WAIT_HINT
 #define SMOE_WAIT_HINT 0x989680
 #endif
