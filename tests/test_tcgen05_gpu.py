@@ -176,10 +176,12 @@ torch.save([x.cpu() for x in outs], sys.argv[1])
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     runs = {}
     for tag, env_add in (("off", {"SMOE_TC_WIDE": "0"}), ("wide4", {"SMOE_TC_WIDE": "1"}),
-                         ("wide1", {"SMOE_TC_WIDE": "1", "SMOE_TC_WIDE_DEFER": "1"})):
+                         ("wide1", {"SMOE_TC_WIDE": "1", "SMOE_TC_WIDE_DEFER": "1"}),
+                         # the wave-lockstep gate only reorders issue in time
+                         ("lockstep", {"SMOE_TC_WIDE": "1", "SMOE_TC_SYNC": "2", "SMOE_TC_SYNC_SLACK": "1"})):
         path = str(tmp_path / f"wide_{tag}.pt")
         subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env_add), timeout=300)
         runs[tag] = torch.load(path)
-    for tag in ("wide4", "wide1"):
+    for tag in ("wide4", "wide1", "lockstep"):
         for i, (u, v) in enumerate(zip(runs["off"], runs[tag])):
             assert torch.equal(u, v), (tag, i)
