@@ -183,6 +183,12 @@ int smoe_group(const void *x, int64_t x_rows, int64_t d, const int32_t *order, i
  *   y_hat [S*J, d], p [S, J] float32 (float64 for SMOE_F64), y [S, d]     */
 int smoe_combine(const void *y_hat, const void *p, int64_t s_rows, int32_t j_cols, int64_t d,
                  int32_t dtype, void *y, void *stream);
+/* the same combine over slot rows held in GROUPED order (a grouped-output
+ * GEMM's layout): y[s] = sum_j p[s,j] * y_hat_grouped[inverse[s*J + j]]
+ * (inverse = the grouped position of each slot, from smoe_route_sort).
+ * Bit-identical to smoe_combine over the slot-ordered rows.              */
+int smoe_combine_grouped(const void *y_hat_grouped, const int32_t *inverse, const void *p, int64_t s_rows,
+                         int32_t j_cols, int64_t d, int32_t dtype, void *y, void *stream);
 
 /* dp (parallel_linear.py:198-206): dp[s,j] = <dy[s], y_hat[s*J + j]>
  *   dy [S, d], y_hat [S*J, d], dp [S, J] float32 (float64 for SMOE_F64)   */
@@ -193,6 +199,10 @@ int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32
  *   g [T*F, d], dx [T, d]                                                 */
 int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, int64_t d,
                        int32_t dtype, void *dx, void *stream);
+/* the same reduce over slot rows in GROUPED order:
+ *   dx[t] = sum_j g_grouped[inverse[t*F + j]]  (bit-identical to smoe_fanout_reduce) */
+int smoe_fanout_reduce_grouped(const void *slot_grads_grouped, const int32_t *inverse, int64_t t_rows,
+                               int32_t fan_out, int64_t d, int32_t dtype, void *dx, void *stream);
 
 /* elementwise activation / derivative (moe_layers.py:75-83), rounded once.
  *   apply: out = act(x);  grad: out = act'(x)                            */

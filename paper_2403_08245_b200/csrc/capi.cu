@@ -28,9 +28,9 @@ int check_launch(const char *what, int launches) {
 size_t route_sort_workspace(int64_t n, int E);
 int route_sort(const int64_t *, int64_t, int, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
 int group(const void *, int64_t, const int32_t *, int64_t, int, const void *, int, void *, cudaStream_t);
-int combine(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int combine(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
 int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
-int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
 int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const void *, int, void *, cudaStream_t);
 int heads_to_grouped(const void *, int64_t, int64_t, int, int, int, const int32_t *, int64_t, int, void *,
@@ -240,7 +240,16 @@ int smoe_combine(const void *y_hat, const void *p, int64_t s_rows, int32_t j_col
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   if (s_rows == 0) return SMOE_OK;
   REQUIRE(y_hat && p && y, SMOE_EINVAL, "combine: null pointer");
-  return combine(y_hat, p, s_rows, j_cols, d, dtype, y, S(stream));
+  return combine(y_hat, p, s_rows, j_cols, d, dtype, y, S(stream), nullptr);
+}
+
+int smoe_combine_grouped(const void *y_hat_grouped, const int32_t *inverse, const void *p, int64_t s_rows,
+                         int32_t j_cols, int64_t d, int32_t dtype, void *y, void *stream) {
+  REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine_grouped: J must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (s_rows == 0) return SMOE_OK;
+  REQUIRE(y_hat_grouped && inverse && p && y, SMOE_EINVAL, "combine_grouped: null pointer");
+  return combine(y_hat_grouped, p, s_rows, j_cols, d, dtype, y, S(stream), inverse);
 }
 
 int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
@@ -294,7 +303,16 @@ int smoe_fanout_reduce(const void *slot_grads, int64_t t_rows, int32_t fan_out, 
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   if (t_rows == 0) return SMOE_OK;
   REQUIRE(slot_grads && dx, SMOE_EINVAL, "fanout_reduce: null pointer");
-  return fanout_reduce(slot_grads, t_rows, fan_out, d, dtype, dx, S(stream));
+  return fanout_reduce(slot_grads, t_rows, fan_out, d, dtype, dx, S(stream), nullptr);
+}
+
+int smoe_fanout_reduce_grouped(const void *slot_grads_grouped, const int32_t *inverse, int64_t t_rows,
+                               int32_t fan_out, int64_t d, int32_t dtype, void *dx, void *stream) {
+  REQUIRE(fan_out >= 1, SMOE_EINVAL, "fan_out must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (t_rows == 0) return SMOE_OK;
+  REQUIRE(slot_grads_grouped && inverse && dx, SMOE_EINVAL, "fanout_reduce_grouped: null pointer");
+  return fanout_reduce(slot_grads_grouped, t_rows, fan_out, d, dtype, dx, S(stream), inverse);
 }
 
 int smoe_apply_activation(const void *x, int64_t numel, int32_t act, int32_t derivative, int32_t dtype,

@@ -182,11 +182,13 @@ int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, i
 }
 
 // ---- combine ---------------------------------------------------------------
+// inv (optional): y_hat holds the slot rows in GROUPED order and slot s*J+j is
+// row inv[s*J+j] (the grouped-output GEMM's layout); null = slot order.
 template <typename T, bool VEC, int JK>
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restrict__ y_hat,
                                                                const typename WOf<T>::type *__restrict__ p,
                                                                int64_t S, int J_, int64_t d,
-                                                               T *__restrict__ y) {
+                                                               T *__restrict__ y, const int32_t *__restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (s >= S) return;
@@ -199,6 +201,12 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
   }
   const T *src = y_hat + s * J * d;
   T *dst = y + s * d;
+  // row of slot s*J+j: (JK > 0) offsets in registers, all k loads in flight
+  int64_t roff[JK > 0 ? JK : 1];
+  if (JK > 0) {
+#pragma unroll
+    for (int j = 0; j < (JK > 0 ? JK : 1); ++j) roff[j] = (inv ? (int64_t)inv[s * J + j] - s * J : j) * d;
+  }
   if (VEC) {
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
@@ -208,7 +216,8 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
 #pragma unroll
       for (int j = 0; j < (JK > 0 ? JK : J); ++j) {
         const A pj = JK > 0 ? pw[j] : (A)p[s * J + j];
-        Vec<T> v = ldv(src + (int64_t)j * d + c);
+        const int64_t ro = JK > 0 ? roff[j] : (inv ? (int64_t)inv[s * J + j] - s * J : j) * d;
+        Vec<T> v = ldv(src + ro + c);
 #pragma unroll
         for (int q = 0; q < N; ++q) acc[q] = fma(pj, Conv<T>::to_acc(v.v[q]), acc[q]);
       }
@@ -220,7 +229,10 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
   } else {
     for (int64_t c = lane; c < d; c += 32) {
       A acc = 0;
-      for (int j = 0; j < J; ++j) acc = fma((A)p[s * J + j], Conv<T>::to_acc(src[(int64_t)j * d + c]), acc);
+      for (int j = 0; j < J; ++j) {
+        const int64_t ro = (inv ? (int64_t)inv[s * J + j] - s * J : j) * d;
+        acc = fma((A)p[s * J + j], Conv<T>::to_acc(src[ro + c]), acc);
+      }
       dst[c] = Conv<T>::from_acc(acc);
     }
   }
@@ -258,11 +270,14 @@ __global__ void __launch_bounds__(kRowThreads) combine_grad_p_kernel(const T *__
 }
 
 // ---- fan-out reduce --------------------------------------------------------
+// inv (optional): g holds the slot rows in GROUPED order (slot t*F+j is row
+// inv[t*F+j]); null = slot order.  Same summation order either way.
 template <typename T, bool VEC, int FK>
 __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__restrict__ g,
                                                                      int64_t Trows, int F_,
                                                                      int64_t d,
-                                                                     T *__restrict__ dx) {
+                                                                     T *__restrict__ dx,
+                                                                     const int32_t *__restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (t >= Trows) return;
@@ -270,6 +285,11 @@ __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__r
   const int F = FK > 0 ? FK : F_;   // FK > 0: compile-time fan-out, all k loads in flight
   const T *src = g + t * F * d;
   T *dst = dx + t * d;
+  int64_t roff[FK > 0 ? FK : 1];
+  if (FK > 0) {
+#pragma unroll
+    for (int j = 0; j < (FK > 0 ? FK : 1); ++j) roff[j] = (inv ? (int64_t)inv[t * F + j] - t * F : j) * d;
+  }
   if (VEC) {
     constexpr int N = Vec<T>::N;
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
@@ -278,7 +298,8 @@ __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__r
       for (int q = 0; q < N; ++q) acc[q] = 0;
 #pragma unroll
       for (int j = 0; j < (FK > 0 ? FK : F); ++j) {
-        Vec<T> v = ldv(src + (int64_t)j * d + c);
+        const int64_t ro = FK > 0 ? roff[j] : (inv ? (int64_t)inv[t * F + j] - t * F : j) * d;
+        Vec<T> v = ldv(src + ro + c);
 #pragma unroll
         for (int q = 0; q < N; ++q) acc[q] += Conv<T>::to_acc(v.v[q]);
       }
@@ -290,7 +311,7 @@ __global__ void __launch_bounds__(kRowThreads) fanout_reduce_kernel(const T *__r
   } else {
     for (int64_t c = lane; c < d; c += 32) {
       A acc = 0;
-      for (int j = 0; j < F; ++j) acc += Conv<T>::to_acc(src[(int64_t)j * d + c]);
+      for (int j = 0; j < F; ++j) acc += Conv<T>::to_acc(src[(inv ? (int64_t)inv[t * F + j] - t * F : j) * d + c]);
       dst[c] = Conv<T>::from_acc(acc);
     }
   }
@@ -340,16 +361,17 @@ int group_inv(const void *x, int64_t t_rows, int64_t d, const int32_t *inv, int 
   return check_launch("group_inv");
 }
 
-int combine(const void *y_hat, const void *p, int64_t S, int J, int64_t d, int dtype, void *y, cudaStream_t st) {
+int combine(const void *y_hat, const void *p, int64_t S, int J, int64_t d, int dtype, void *y, cudaStream_t st,
+            const int32_t *inv) {
   if (S == 0 || d == 0) return SMOE_OK;
   SMOE_DTYPE_DISPATCH(dtype, {
     using W = typename WOf<T>::type;
     if (vec_ok(y_hat, d, sizeof(T)) && vec_ok(y, d, sizeof(T)))
       SMOE_FANOUT_DISPATCH(J, (combine_kernel<T, true, FKC><<<row_blocks(S), kRowThreads, 0, st>>>(
-                                  (const T *)y_hat, (const W *)p, S, J, d, (T *)y)));
+                                  (const T *)y_hat, (const W *)p, S, J, d, (T *)y, inv)));
     else
       combine_kernel<T, false, 0><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)y_hat, (const W *)p, S, J, d,
-                                                                         (T *)y);
+                                                                         (T *)y, inv);
   });
   return check_launch("combine");
 }
@@ -387,14 +409,16 @@ int dp_from_partials(const float *part, int64_t n, int parts, const int32_t *ord
   return check_launch("dp_from_partials");
 }
 
-int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx, cudaStream_t st) {
+int fanout_reduce(const void *g, int64_t Trows, int F, int64_t d, int dtype, void *dx, cudaStream_t st,
+                  const int32_t *inv) {
   if (Trows == 0 || d == 0) return SMOE_OK;
   SMOE_DTYPE_DISPATCH(dtype, {
     if (vec_ok(g, d, sizeof(T)) && vec_ok(dx, d, sizeof(T)))
       SMOE_FANOUT_DISPATCH(F, (fanout_reduce_kernel<T, true, FKC><<<row_blocks(Trows), kRowThreads, 0, st>>>(
-                                  (const T *)g, Trows, F, d, (T *)dx)));
+                                  (const T *)g, Trows, F, d, (T *)dx, inv)));
     else
-      fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx);
+      fanout_reduce_kernel<T, false, 0><<<row_blocks(Trows), kRowThreads, 0, st>>>((const T *)g, Trows, F, d, (T *)dx,
+                                                                                   inv);
   });
   return check_launch("fanout_reduce");
 }

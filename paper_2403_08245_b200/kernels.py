@@ -526,16 +526,26 @@ def group_xty_scattered(
 
 # ---- row kernels used by parallel_linear (not in the reference's kernels.py) ----
 
-def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Y[s] = sum_i p[s, i] * Y_hat[s*j + i]  (parallel_linear.py:69-73)."""
+def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = None,
+            inverse: torch.Tensor | None = None) -> torch.Tensor:
+    """Y[s] = sum_i p[s, i] * Y_hat[s*j + i]  (parallel_linear.py:69-73).
+
+    inverse: Y_hat holds the slot rows in grouped order (a grouped-output
+    GEMM's layout) and slot r is row inverse[r]; same result bit for bit."""
     s, j = p.shape
     y_hat = _cuda(y_hat, "y_hat")
     p32 = _cuda(p.to(_wdtype(y_hat)), "p")
     if out is None:
         out = torch.empty((s, y_hat.shape[1]), dtype=y_hat.dtype, device=y_hat.device)
     t0 = _lt.begin()
-    st = _lib.load().smoe_combine(y_hat.data_ptr(), p32.data_ptr(), s, j, y_hat.shape[1],
-                                  _dtype_id(y_hat), out.data_ptr(), _stream(y_hat))
+    if inverse is not None:
+        inv = _cuda(inverse, "inverse").to(torch.int32).contiguous()
+        require_dims(inv.numel() == s * j == y_hat.shape[0], "inverse vs slot rows", (inv.numel(),), (s * j,))
+        st = _lib.load().smoe_combine_grouped(y_hat.data_ptr(), inv.data_ptr(), p32.data_ptr(), s, j,
+                                              y_hat.shape[1], _dtype_id(y_hat), out.data_ptr(), _stream(y_hat))
+    else:
+        st = _lib.load().smoe_combine(y_hat.data_ptr(), p32.data_ptr(), s, j, y_hat.shape[1],
+                                      _dtype_id(y_hat), out.data_ptr(), _stream(y_hat))
     _lt.end("combine", t0)
     _lib.check(st, "combine")
     return out
@@ -553,15 +563,24 @@ def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int) -> tor
     return dp
 
 
-def fanout_reduce(slot_grads: torch.Tensor, fan_out: int, out: torch.Tensor | None = None) -> torch.Tensor:
-    """dX[t] = sum_j G[t*fan_out + j]  (parallel_linear.py:259-266)."""
+def fanout_reduce(slot_grads: torch.Tensor, fan_out: int, out: torch.Tensor | None = None,
+                  inverse: torch.Tensor | None = None) -> torch.Tensor:
+    """dX[t] = sum_j G[t*fan_out + j]  (parallel_linear.py:259-266).
+
+    inverse: G holds the slot rows in grouped order (slot r is row inverse[r])."""
     g = _cuda(slot_grads, "slot_grads")
     t = g.shape[0] // fan_out
     if out is None:
         out = torch.empty((t, g.shape[1]), dtype=g.dtype, device=g.device)
     t0 = _lt.begin()
-    st = _lib.load().smoe_fanout_reduce(g.data_ptr(), t, fan_out, g.shape[1], _dtype_id(g),
-                                        out.data_ptr(), _stream(g))
+    if inverse is not None:
+        inv = _cuda(inverse, "inverse").to(torch.int32).contiguous()
+        require_dims(inv.numel() == g.shape[0], "inverse vs slot rows", (inv.numel(),), (g.shape[0],))
+        st = _lib.load().smoe_fanout_reduce_grouped(g.data_ptr(), inv.data_ptr(), t, fan_out, g.shape[1],
+                                                    _dtype_id(g), out.data_ptr(), _stream(g))
+    else:
+        st = _lib.load().smoe_fanout_reduce(g.data_ptr(), t, fan_out, g.shape[1], _dtype_id(g),
+                                            out.data_ptr(), _stream(g))
     _lt.end("fanout_reduce", t0)
     _lib.check(st, "fanout_reduce")
     return out

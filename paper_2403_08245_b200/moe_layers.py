@@ -141,6 +141,14 @@ class SmoeMlpContext:
 _SCALED = os.environ.get("SMOE_MLP_SCALED", "1") != "0"
 
 
+# SMOE_GROUPED_REDUCE=1: the k-summed GEMMs (layer 2, the input gradient) write
+# grouped rows (TMA slab stores) and the k-sum reads them through the inverse
+# permutation.  Measured against scattered-row outputs (alternating, one box):
+# C1 906-910 k vs 907-909 k tok/s, C2 1.593-1.598 M vs 1.582-1.600 M — the
+# staged scattered-row epilogue is not what limits those GEMMs; off.
+_GROUPED_REDUCE = os.environ.get("SMOE_GROUPED_REDUCE", "0") == "1"
+
+
 def set_scaled(enabled: bool) -> bool:
     """Select the routing-weight-scaled MLP path (True) or the literal one; returns the previous value."""
     global _SCALED
@@ -191,8 +199,14 @@ def smoe_mlp_forward(
         hp = torch.empty((n, de), dtype=x.dtype, device=x.device)
         K.scatter2scatter_scaled(x, w1, order, k, SCATTERED_TO_GROUPED, row_scale=p_flat, activation=activation,
                                  out=h_pre, act_out=hp)
-        y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_SCATTERED)
-        y = K.fanout_reduce(y_hat_p, k)
+        if _GROUPED_REDUCE:
+            # layer 2 writes grouped rows (whole 32-row slabs leave by TMA) and the
+            # k-sum gathers each token's rows through the inverse permutation
+            y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_GROUPED)
+            y = K.fanout_reduce(y_hat_p, k, inverse=order.inverse())
+        else:
+            y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_SCATTERED)
+            y = K.fanout_reduce(y_hat_p, k)
         if ledger:
             ledger.alloc("mlp.hidden.y", n, de, "forward")
             ledger.alloc("mlp.h_preactivation", n, de, "backward")
@@ -273,8 +287,12 @@ def _scaled_backward(ctx: SmoeMlpContext, dy: torch.Tensor, on_dx=None) -> SmoeM
                                   activation=ctx.activation, out=st.hp, act_grad_of=ctx.h_pre,
                                   dp_partials=parts, transpose_w=True)
     dp = K.dp_from_partials(parts, order, t, k)
-    slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_SCATTERED, transpose_w=True, out=dyg)
-    dx = K.fanout_reduce(slot, k)
+    if _GROUPED_REDUCE:
+        slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_GROUPED, transpose_w=True, out=dyg)
+        dx = K.fanout_reduce(slot, k, inverse=order.inverse())
+    else:
+        slot = K.scatter2scatter(dh, st.w1, order, 1, GROUPED_TO_SCATTERED, transpose_w=True, out=dyg)
+        dx = K.fanout_reduce(slot, k)
     if on_dx is not None:
         on_dx(dx, dp)
     if pl._gather_ok(de, st.x) and order.num_experts <= 128:

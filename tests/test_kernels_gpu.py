@@ -329,3 +329,19 @@ def test_fp32_check_mode_accumulates_in_64_bit():
     dw = sm.group_xty(t(np.array([[2.0 ** 24], [1.0], [-(2.0 ** 24)]], dtype=np.float32)),
                       t(np.ones((3, 1), dtype=np.float32)), order_of(np.zeros((3, 1), dtype=np.int64), 1))
     assert float(dw[0, 0, 0]) == 1.0
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
+def test_grouped_row_reductions_match_slot_order(k):
+    """fanout_reduce / combine over grouped rows (through the inverse
+    permutation) are bit-identical to the slot-ordered kernels."""
+    g = torch.Generator(device="cuda").manual_seed(k)
+    tokens, e, d = 777, 8, 264
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+    order = sm.compute_grouped_order(routing)
+    slots = (torch.rand((tokens * k, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    grouped = slots[order.o.long()]                     # row i = slot o[i]
+    inv = order.inverse()
+    assert torch.equal(sm.kernels.fanout_reduce(grouped, k, inverse=inv), sm.kernels.fanout_reduce(slots, k))
+    p = routing.p.float()
+    assert torch.equal(sm.kernels.combine(p, grouped, inverse=inv), sm.kernels.combine(p, slots))
