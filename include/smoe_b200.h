@@ -194,6 +194,9 @@ int smoe_combine_grouped(const void *y_hat_grouped, const int32_t *inverse, cons
  *   dy [S, d], y_hat [S*J, d], dp [S, J] float32 (float64 for SMOE_F64)   */
 int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32_t j_cols,
                         int64_t d, int32_t dtype, void *dp, void *stream);
+/* the same over slot rows in GROUPED order: dp[s,j] = <dy[s], y_hat_grouped[inverse[s*J + j]]> */
+int smoe_combine_grad_p_grouped(const void *dy, const void *y_hat_grouped, const int32_t *inverse, int64_t s_rows,
+                                int32_t j_cols, int64_t d, int32_t dtype, void *dp, void *stream);
 
 /* fan-out reduce (parallel_linear.py:259-266): dx[t] = sum_j g[t*F + j]
  *   g [T*F, d], dx [T, d]                                                 */

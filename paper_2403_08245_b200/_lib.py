@@ -48,6 +48,7 @@ SIGNATURES = {
     "smoe_fanout_reduce": (_c.c_int, [_vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_fanout_reduce_grouped": (_c.c_int, [_vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_combine_grouped": (_c.c_int, [_vp, _vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
+    "smoe_combine_grad_p_grouped": (_c.c_int, [_vp, _vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp]),
     "smoe_apply_activation": (_c.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "smoe_ipc_handle_bytes": (_sz, []),
     "smoe_ipc_get_handle": (_c.c_int, [_vp, _vp, _c.POINTER(_c.c_int64)]),

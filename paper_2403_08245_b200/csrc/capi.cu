@@ -29,7 +29,7 @@ size_t route_sort_workspace(int64_t n, int E);
 int route_sort(const int64_t *, int64_t, int, int32_t *, int32_t *, int32_t *, int32_t *, void *, size_t, cudaStream_t);
 int group(const void *, int64_t, const int32_t *, int64_t, int, const void *, int, void *, cudaStream_t);
 int combine(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
-int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t);
+int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
 int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const void *, int, void *, cudaStream_t);
@@ -258,7 +258,16 @@ int smoe_combine_grad_p(const void *dy, const void *y_hat, int64_t s_rows, int32
   REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
   if (s_rows == 0) return SMOE_OK;
   REQUIRE(dy && y_hat && dp, SMOE_EINVAL, "combine_grad_p: null pointer");
-  return combine_grad_p(dy, y_hat, s_rows, j_cols, d, dtype, dp, S(stream));
+  return combine_grad_p(dy, y_hat, s_rows, j_cols, d, dtype, dp, S(stream), nullptr);
+}
+
+int smoe_combine_grad_p_grouped(const void *dy, const void *y_hat_grouped, const int32_t *inverse, int64_t s_rows,
+                                int32_t j_cols, int64_t d, int32_t dtype, void *dp, void *stream) {
+  REQUIRE(j_cols >= 1, SMOE_EINVAL, "combine_grad_p_grouped: J must be >= 1");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (s_rows == 0) return SMOE_OK;
+  REQUIRE(dy && y_hat_grouped && inverse && dp, SMOE_EINVAL, "combine_grad_p_grouped: null pointer");
+  return combine_grad_p(dy, y_hat_grouped, s_rows, j_cols, d, dtype, dp, S(stream), inverse);
 }
 
 int32_t smoe_dp_parts(int64_t d_out) { return (int32_t)(2 * ((d_out + 255) / 256)); }

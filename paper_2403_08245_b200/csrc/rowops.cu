@@ -240,18 +240,20 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const T *__restric
 
 // ---- dp --------------------------------------------------------------------
 // One warp per combine row s; J partial dot products reduced with shuffles.
+// inv (optional): y_hat in grouped order, slot s*J+j is row inv[s*J+j].
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kRowThreads) combine_grad_p_kernel(const T *__restrict__ dy,
                                                                       const T *__restrict__ y_hat,
                                                                       int64_t S, int J, int64_t d,
-                                                                      typename WOf<T>::type *__restrict__ dp) {
+                                                                      typename WOf<T>::type *__restrict__ dp,
+                                                                      const int32_t *__restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (s >= S) return;
   using A = typename AccOf<T>::type;
   const T *g = dy + s * d;
   for (int j = 0; j < J; ++j) {
-    const T *yh = y_hat + (s * J + j) * d;
+    const T *yh = y_hat + (inv ? (int64_t)inv[s * J + j] : s * J + j) * d;
     A acc = 0;
     if (VEC) {
       constexpr int N = Vec<T>::N;
@@ -377,16 +379,16 @@ int combine(const void *y_hat, const void *p, int64_t S, int J, int64_t d, int d
 }
 
 int combine_grad_p(const void *dy, const void *y_hat, int64_t S, int J, int64_t d, int dtype, void *dp,
-                   cudaStream_t st) {
+                   cudaStream_t st, const int32_t *inv) {
   if (S == 0) return SMOE_OK;
   SMOE_DTYPE_DISPATCH(dtype, {
     using W = typename WOf<T>::type;
     if (vec_ok(dy, d, sizeof(T)) && vec_ok(y_hat, d, sizeof(T)))
       combine_grad_p_kernel<T, true><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d,
-                                                                            (W *)dp);
+                                                                            (W *)dp, inv);
     else
       combine_grad_p_kernel<T, false><<<row_blocks(S), kRowThreads, 0, st>>>((const T *)dy, (const T *)y_hat, S, J, d,
-                                                                             (W *)dp);
+                                                                             (W *)dp, inv);
   });
   return check_launch("combine_grad_p");
 }

@@ -551,13 +551,22 @@ def combine(p: torch.Tensor, y_hat: torch.Tensor, out: torch.Tensor | None = Non
     return out
 
 
-def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int) -> torch.Tensor:
-    """dp[s, i] = <dY[s], Y_hat[s*j + i]>  (parallel_linear.py:198-206), float32."""
+def combine_grad_p(dy: torch.Tensor, y_hat: torch.Tensor, s: int, j: int,
+                   inverse: torch.Tensor | None = None) -> torch.Tensor:
+    """dp[s, i] = <dY[s], Y_hat[s*j + i]>  (parallel_linear.py:198-206), float32.
+
+    inverse: Y_hat holds the slot rows in grouped order (slot r is row inverse[r])."""
     dy, y_hat = _cuda(dy, "dy"), _cuda(y_hat, "y_hat")
     dp = torch.empty((s, j), dtype=_wdtype(dy), device=dy.device)
     t0 = _lt.begin()
-    st = _lib.load().smoe_combine_grad_p(dy.data_ptr(), y_hat.data_ptr(), s, j, dy.shape[1],
-                                         _dtype_id(dy), dp.data_ptr(), _stream(dy))
+    if inverse is not None:
+        inv = _cuda(inverse, "inverse").to(torch.int32).contiguous()
+        require_dims(inv.numel() == s * j == y_hat.shape[0], "inverse vs slot rows", (inv.numel(),), (s * j,))
+        st = _lib.load().smoe_combine_grad_p_grouped(dy.data_ptr(), y_hat.data_ptr(), inv.data_ptr(), s, j,
+                                                     dy.shape[1], _dtype_id(dy), dp.data_ptr(), _stream(dy))
+    else:
+        st = _lib.load().smoe_combine_grad_p(dy.data_ptr(), y_hat.data_ptr(), s, j, dy.shape[1],
+                                             _dtype_id(dy), dp.data_ptr(), _stream(dy))
     _lt.end("combine_grad_p", t0)
     _lib.check(st, "combine_grad_p")
     return dp

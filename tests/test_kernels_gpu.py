@@ -345,3 +345,6 @@ def test_grouped_row_reductions_match_slot_order(k):
     assert torch.equal(sm.kernels.fanout_reduce(grouped, k, inverse=inv), sm.kernels.fanout_reduce(slots, k))
     p = routing.p.float()
     assert torch.equal(sm.kernels.combine(p, grouped, inverse=inv), sm.kernels.combine(p, slots))
+    dy = (torch.rand((tokens, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    assert torch.equal(sm.kernels.combine_grad_p(dy, grouped, tokens, k, inverse=inv),
+                       sm.kernels.combine_grad_p(dy, slots, tokens, k))
