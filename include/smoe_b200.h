@@ -160,6 +160,15 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
  * pass replaces the head->slot permute and the grouped copy of the slot rows. */
 int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
                           int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream);
+/* the reverse: heads[batch][hh * k + j][t % seq_len][:] = grouped[i][hh * d_head :] for the
+ * slot s = order[i] — grouped slot rows (a grouped-output GEMM's layout) to the
+ * attention core's head layout. */
+int smoe_grouped_to_heads(const void *grouped, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
+                          int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *heads, void *stream);
+/* out[i] = x_grouped[i] * weights[order[i]] (the routing weight of each grouped
+ * row's slot), rounded once: group()'s weighting for rows already grouped. */
+int smoe_scale_grouped_rows(const void *x_grouped, int64_t d, const int32_t *order, int64_t n, const void *weights,
+                            int32_t dtype, void *out, void *stream);
 
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,
                    const void *weights, int32_t dtype, void *out, void *stream);

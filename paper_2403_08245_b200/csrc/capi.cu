@@ -33,6 +33,8 @@ int combine_grad_p(const void *, const void *, int64_t, int, int64_t, int, void 
 int fanout_reduce(const void *, int64_t, int, int64_t, int, void *, cudaStream_t, const int32_t *);
 int dp_from_partials(const float *, int64_t, int, const int32_t *, float *, cudaStream_t);
 int group_inv(const void *, int64_t, int64_t, const int32_t *, int, const void *, int, void *, cudaStream_t);
+int grouped_to_heads(const void *, int64_t, int, int, int, const int32_t *, int64_t, int, void *, cudaStream_t);
+int scale_grouped_rows(const void *, int64_t, const int32_t *, int64_t, const void *, int, void *, cudaStream_t);
 int heads_to_grouped(const void *, int64_t, int64_t, int, int, int, const int32_t *, int64_t, int, void *,
                      cudaStream_t);
 int tc_scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
@@ -223,6 +225,24 @@ int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int
   if (n == 0) return SMOE_OK;
   REQUIRE(heads && order && out, SMOE_EINVAL, "heads_to_grouped: null pointer");
   return heads_to_grouped(heads, batch, seq_len, k, heads_per_slot, d_head, order, n, dtype, out, S(stream));
+}
+
+int smoe_grouped_to_heads(const void *grouped, int64_t batch, int64_t seq_len, int32_t k, int32_t h, int32_t d_head,
+                          const int32_t *order, int64_t n, int32_t dtype, void *heads, void *stream) {
+  REQUIRE(k >= 1 && h >= 1 && d_head >= 1 && seq_len >= 1, SMOE_EINVAL, "grouped_to_heads: bad dimensions");
+  REQUIRE(n == batch * seq_len * k, SMOE_ESHAPE, "grouped_to_heads: n must equal batch * seq_len * k");
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(grouped && order && heads, SMOE_EINVAL, "grouped_to_heads: null pointer");
+  return grouped_to_heads(grouped, seq_len, k, h, d_head, order, n, dtype, heads, S(stream));
+}
+
+int smoe_scale_grouped_rows(const void *x_grouped, int64_t d, const int32_t *order, int64_t n, const void *weights,
+                            int32_t dtype, void *out, void *stream) {
+  REQUIRE(valid_dtype(dtype), SMOE_EINVAL, "unsupported dtype");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(x_grouped && order && weights && out, SMOE_EINVAL, "scale_grouped_rows: null pointer");
+  return scale_grouped_rows(x_grouped, d, order, n, weights, dtype, out, S(stream));
 }
 
 int smoe_group_inv(const void *x, int64_t x_rows, int64_t d, const int32_t *inverse, int32_t fan_out,

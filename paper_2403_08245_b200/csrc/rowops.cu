@@ -141,29 +141,112 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
 // One warp per grouped row i: slot s = order[i], token t = s / k, choice j;
 // the row's d_proj = h * d_head values come from head hh * k + j of t's
 // sequence position, d_head contiguous elements per head (16-byte chunks).
+// Slot rows <-> the attention core's head layout.  One warp moves kHeadRows
+// grouped rows per pass: every lane issues its 16-byte loads for all of them
+// before the first store (a row is only h * d_head * 2 B = 1 KB at C3, so one
+// row per warp left the copy latency-bound at ~4.4 TB/s).
+//   TO_HEADS = false: out[i] (grouped row) <- heads[b][hh*k + j][pos][:]
+//   TO_HEADS = true : heads[b][hh*k + j][pos][:] <- grouped[i]
+constexpr int kHeadRows = 4;
+template <typename T, bool TO_HEADS>
+__global__ void __launch_bounds__(kRowThreads) heads_grouped_kernel(const T *__restrict__ src, int64_t seq_len,
+                                                                    int k, int h, int dh,
+                                                                    const int32_t *__restrict__ order, int64_t n,
+                                                                    T *__restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * kHeadRows;
+  constexpr int N = 16 / sizeof(T);           // elements per 16-byte chunk
+  const int cph = dh / N;                     // chunks per head
+  const int cpr = h * cph;                    // chunks per row
+  // lane r < kHeadRows resolves row i0 + r once: its head-layout base (head 0)
+  int64_t hb = -1;
+  if (lane < kHeadRows && i0 + lane < n) {
+    const int64_t s = order[i0 + lane];
+    const int64_t t = s / k;
+    const int j = (int)(s - t * k);
+    const int64_t b = t / seq_len, pos = t - b * seq_len;
+    hb = ((b * h * k + j) * seq_len + pos) * (int64_t)dh;
+  }
+  const int64_t head_stride = (int64_t)k * seq_len * dh;   // head hh -> hh + 1 of one slot
+  const int total = kHeadRows * cpr;
+  for (int c0 = 0; c0 < total; c0 += 32 * 8) {
+    uint4 v[8];
+    int64_t doff[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      const int r = c < total ? c / cpr : 0;
+      const int64_t base = __shfl_sync(0xffffffffu, hb, r);
+      doff[u] = -1;
+      if (c >= total || base < 0) continue;
+      const int cc = c - r * cpr;
+      const int hh = cc / cph, q = cc - hh * cph;
+      const int64_t hoff = base + hh * head_stride + q * N;
+      const int64_t goff = (i0 + r) * (int64_t)h * dh + (int64_t)cc * N;
+      v[u] = __ldg(reinterpret_cast<const uint4 *>(src + (TO_HEADS ? goff : hoff)));
+      doff[u] = TO_HEADS ? hoff : goff;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (doff[u] >= 0) *reinterpret_cast<uint4 *>(dst + doff[u]) = v[u];
+  }
+}
+
+// out[i] = x[i] * w[order[i]] over grouped rows (the routing weight of each
+// grouped row's slot), rounded once.
 template <typename T>
-__global__ void __launch_bounds__(kRowThreads) heads_to_grouped_kernel(const T *__restrict__ heads, int64_t seq_len,
-                                                                       int k, int h, int dh,
-                                                                       const int32_t *__restrict__ order, int64_t n,
-                                                                       T *__restrict__ out) {
+__global__ void __launch_bounds__(kRowThreads) scale_grouped_rows_kernel(const T *__restrict__ x, int64_t d,
+                                                                         const int32_t *__restrict__ order,
+                                                                         int64_t n,
+                                                                         const typename WOf<T>::type *__restrict__ w,
+                                                                         T *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (i >= n) return;
-  const int64_t s = order[i];
-  const int64_t t = s / k;
-  const int j = (int)(s - t * k);
-  const int64_t b = t / seq_len, pos = t - b * seq_len;
-  constexpr int N = 16 / sizeof(T);           // elements per 16-byte chunk
-  const int cph = dh / N;                     // chunks per head
-  T *dst = out + i * (int64_t)h * dh;
-  for (int c = lane; c < h * cph; c += 32) {
-    const int hh = c / cph, q = c - hh * cph;
-    const T *src = heads + (((b * h + hh) * k + j) * seq_len + pos) * (int64_t)dh + q * N;
-    *reinterpret_cast<uint4 *>(dst + hh * dh + q * N) = __ldg(reinterpret_cast<const uint4 *>(src));
+  using A = typename AccOf<T>::type;
+  const A wi = (A)w[order[i]];
+  const T *src = x + i * d;
+  T *dst = out + i * d;
+  constexpr int N = Vec<T>::N;
+  for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
+    Vec<T> v = ldv(src + c), o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) o.v[q] = Conv<T>::from_acc(Conv<T>::to_acc(v.v[q]) * wi);
+    stv(dst + c, o);
   }
 }
 
 static inline unsigned row_blocks(int64_t rows);
+
+int grouped_to_heads(const void *grouped, int64_t seq_len, int k, int h, int dh, const int32_t *order, int64_t n,
+                     int dtype, void *heads, cudaStream_t st) {
+  if (dtype == SMOE_F64) return fail(SMOE_ENOTSUP, "grouped_to_heads: bf16 / fp32 only");
+  const int esz = dtype == SMOE_BF16 ? 2 : 4;
+  if ((dh * esz) % 16 || (reinterpret_cast<uintptr_t>(heads) | reinterpret_cast<uintptr_t>(grouped)) % 16)
+    return fail(SMOE_ENOTSUP, "grouped_to_heads: d_head * element size must be a multiple of 16 bytes (aligned)");
+  if (n == 0) return SMOE_OK;
+  if (dtype == SMOE_BF16)
+    heads_grouped_kernel<__nv_bfloat16, true><<<row_blocks((n + kHeadRows - 1) / kHeadRows), kRowThreads, 0, st>>>(
+        (const __nv_bfloat16 *)grouped, seq_len, k, h, dh, order, n, (__nv_bfloat16 *)heads);
+  else
+    heads_grouped_kernel<float, true><<<row_blocks((n + kHeadRows - 1) / kHeadRows), kRowThreads, 0, st>>>(
+        (const float *)grouped, seq_len, k, h, dh, order, n, (float *)heads);
+  return check_launch("grouped_to_heads");
+}
+
+int scale_grouped_rows(const void *x, int64_t d, const int32_t *order, int64_t n, const void *w, int dtype, void *out,
+                       cudaStream_t st) {
+  if (n == 0 || d == 0) return SMOE_OK;
+  if (!vec_ok(x, d, dtype == SMOE_BF16 ? 2 : dtype == SMOE_F32 ? 4 : 8) ||
+      !vec_ok(out, d, dtype == SMOE_BF16 ? 2 : dtype == SMOE_F32 ? 4 : 8))
+    return fail(SMOE_ENOTSUP, "scale_grouped_rows: rows must be 16-byte aligned");
+  SMOE_DTYPE_DISPATCH(dtype, {
+    using W = typename WOf<T>::type;
+    scale_grouped_rows_kernel<T><<<row_blocks(n), kRowThreads, 0, st>>>((const T *)x, d, order, n, (const W *)w,
+                                                                        (T *)out);
+  });
+  return check_launch("scale_grouped_rows");
+}
 
 int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, int h, int dh, const int32_t *order,
                      int64_t n, int dtype, void *out, cudaStream_t st) {
@@ -173,11 +256,11 @@ int heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int k, i
   if ((dh * esz) % 16 || (reinterpret_cast<uintptr_t>(heads) | reinterpret_cast<uintptr_t>(out)) % 16)
     return fail(SMOE_ENOTSUP, "heads_to_grouped: d_head * element size must be a multiple of 16 bytes (aligned)");
   if (dtype == SMOE_BF16)
-    heads_to_grouped_kernel<__nv_bfloat16><<<row_blocks(n), kRowThreads, 0, st>>>(
+    heads_grouped_kernel<__nv_bfloat16, false><<<row_blocks((n + kHeadRows - 1) / kHeadRows), kRowThreads, 0, st>>>(
         (const __nv_bfloat16 *)heads, seq_len, k, h, dh, order, n, (__nv_bfloat16 *)out);
   else
-    heads_to_grouped_kernel<float><<<row_blocks(n), kRowThreads, 0, st>>>((const float *)heads, seq_len, k, h, dh,
-                                                                         order, n, (float *)out);
+    heads_grouped_kernel<float, false><<<row_blocks((n + kHeadRows - 1) / kHeadRows), kRowThreads, 0, st>>>(
+        (const float *)heads, seq_len, k, h, dh, order, n, (float *)out);
   return check_launch("heads_to_grouped");
 }
 

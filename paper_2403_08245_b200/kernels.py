@@ -463,6 +463,42 @@ def heads_to_grouped(heads: torch.Tensor, order: GroupedOrder, k: int) -> torch.
     return out
 
 
+def grouped_to_heads(grouped: torch.Tensor, order: GroupedOrder, k: int, batch: int, seq_len: int,
+                     d_head: int) -> torch.Tensor:
+    """The attention core's head layout (batch, h*k, seq_len, d_head) from grouped
+    slot rows (n, h*d_head) — the reverse of heads_to_grouped."""
+    grouped = _cuda(grouped, "grouped").contiguous()
+    n = order.num_slots
+    require_dims(grouped.shape[0] == n == batch * seq_len * k, "grouped rows vs batch*seq_len*k",
+                 (grouped.shape[0],), (batch * seq_len * k,))
+    if grouped.shape[1] % d_head:
+        raise ValueError(f"row width {grouped.shape[1]} is not divisible by d_head {d_head}")
+    h = grouped.shape[1] // d_head
+    heads = torch.empty((batch, h * k, seq_len, d_head), dtype=grouped.dtype, device=grouped.device)
+    t0 = _lt.begin()
+    st = _lib.load().smoe_grouped_to_heads(grouped.data_ptr(), batch, seq_len, k, h, d_head, order.o.data_ptr(), n,
+                                           _dtype_id(grouped), heads.data_ptr(), _stream(grouped))
+    _lt.end("grouped_to_heads", t0)
+    _lib.check(st, "grouped_to_heads")
+    return heads
+
+
+def scale_grouped_rows(x_grouped: torch.Tensor, order: GroupedOrder, weights: torch.Tensor,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[i] = x_grouped[i] * weights[o[i]] (group()'s weighting for rows already grouped)."""
+    x = _cuda(x_grouped, "x_grouped").contiguous()
+    require_dims(x.shape[0] == order.num_slots, "grouped rows vs slots", (x.shape[0],), (order.num_slots,))
+    w = _cuda(weights.reshape(-1).to(_wdtype(x)), "weights").contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    t0 = _lt.begin()
+    st = _lib.load().smoe_scale_grouped_rows(x.data_ptr(), x.shape[1], order.o.data_ptr(), x.shape[0], w.data_ptr(),
+                                             _dtype_id(x), out.data_ptr(), _stream(x))
+    _lt.end("scale_grouped_rows", t0)
+    _lib.check(st, "scale_grouped_rows")
+    return out
+
+
 def dp_parts(d_out: int) -> int:
     return int(_lib.load().smoe_dp_parts(d_out))
 

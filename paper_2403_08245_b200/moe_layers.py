@@ -392,7 +392,10 @@ def init_momha_weights(config: MomhaConfig, seed: int, dtype=torch.float32, devi
 
 
 _GQA = os.environ.get("SMOE_MOMHA_GQA", "1") != "0"
-_GROUPED_DQ = os.environ.get("SMOE_MOMHA_GROUPED_DQ", "1") != "0"
+
+
+# SMOE_MOMHA_GROUPED=0: slot rows in slot order around the attention core (A/B)
+_MOMHA_GROUPED = os.environ.get("SMOE_MOMHA_GROUPED", "1") != "0"
 
 
 def _contig16(t: torch.Tensor) -> torch.Tensor:
@@ -508,18 +511,28 @@ def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: Group
                          f"expected {n} tokens with k={config.k}")
     keys = _mm(x, weights.wk)
     values = _mm(x, weights.wv)
-    q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=SCATTERED_TO_SCATTERED,
+    fused = (training and x.dtype == torch.bfloat16 and config.d_head % 8 == 0
+             and (weights.wq.shape[2] % config.d_head) == 0)
+    grouped = fused and _MOMHA_GROUPED
+    # bf16 training: the slot rows around the attention core live in GROUPED
+    # order — the query projection writes grouped rows (TMA slab stores), one
+    # pass moves them into the core's head layout, one pass brings the core's
+    # output back as grouped rows, and the output projection then reads them by
+    # TMA (no row gather) and its backward stays in grouped order too
+    q_layout = SCATTERED_TO_GROUPED if grouped else SCATTERED_TO_SCATTERED
+    q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=q_layout,
                               tile=tile, training=training, ledger=ledger, name="momha.query")
     attn_graph = None
-    if training and q.dtype == torch.bfloat16 and config.d_head % 8 == 0:
+    o_layout = SCATTERED_TO_SCATTERED
+    if fused:
         # keep the attention core's autograd graph for the backward instead of
         # recomputing it (attention_backward, the reference's :330-377 form)
-        require_dims(q.shape[1] % config.d_head == 0, "projection width vs d_head", (q.shape[1],),
-                     (config.d_head,))
-        kk, dh = q.shape[0] // n, config.d_head
+        kk, dh = config.k, config.d_head
         b, h = n // seq_len, q.shape[1] // dh
-        # slot rows (b, S, k, h, d) <-> SDPA heads (b, h*k, S, d) by 16-byte-element copies
-        qh = _contig16(q.view(b, seq_len, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, seq_len, dh)
+        if grouped:
+            qh = K.grouped_to_heads(q, order, kk, b, seq_len, dh)
+        else:   # slot rows (b, S, k, h, d) -> heads (b, h*k, S, d) by 16-byte-element copies
+            qh = _contig16(q.view(b, seq_len, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, seq_len, dh)
         with torch.enable_grad():
             qv = qh.requires_grad_(True)
             kv = keys.view(b, seq_len, h, dh).transpose(1, 2).detach().requires_grad_(True)
@@ -527,11 +540,15 @@ def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: Group
             out = torch.nn.functional.scaled_dot_product_attention(qv, kv, vv, is_causal=config.causal,
                                                                    enable_gqa=kk > 1)
         attn_graph = (qv, kv, vv, out, (b, seq_len, kk, h, dh))
-        attn_out = _contig16(out.detach().view(b, h, kk, seq_len, dh).permute(0, 3, 2, 1, 4)).view(n * kk, h * dh)
+        if grouped:
+            attn_out = K.heads_to_grouped(out.detach().contiguous(), order, kk)
+            o_layout = GROUPED_TO_SCATTERED
+        else:
+            attn_out = _contig16(out.detach().view(b, h, kk, seq_len, dh).permute(0, 3, 2, 1, 4)).view(n * kk, h * dh)
     else:
         attn_out = attention(q, keys, values, None, seq_len, config.d_head, config.causal)
     y, output_ctx = pl.forward(attn_out, weights.wo, order, p=routing.p, fan_out=1,
-                               layout=SCATTERED_TO_SCATTERED, tile=tile, training=training, ledger=ledger,
+                               layout=o_layout, tile=tile, training=training, ledger=ledger,
                                name="momha.output")
     if not training:
         return y, None
@@ -546,16 +563,15 @@ def momha_backward(ctx: MomhaContext, dy, *, tile: TileConfig | None = None, led
     if ctx.attn_graph is not None:
         qv, kv, vv, out, (b, sl, kk, h, dh) = ctx.attn_graph
         ctx.attn_graph = None
-        d_out = _contig16(g_o.dx.to(out.dtype).view(b, sl, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, sl, dh)
-        dqh, dkh, dvh = torch.autograd.grad(out, (qv, kv, vv), d_out)
-        if _GROUPED_DQ and dqh.is_contiguous() and (dh * dqh.element_size()) % 16 == 0:
-            # the query gradient goes straight from the head layout to grouped
-            # rows: the query projection's backward then reads it by TMA (no
-            # gathers, parallel_linear.py:208-222 with a grouped dY)
-            dq = K.heads_to_grouped(dqh, ctx.query_ctx.order, kk)
-            ctx.query_ctx.y_was_grouped = True
+        if ctx.output_ctx.x_was_grouped:   # the output projection's input gradient comes back as grouped rows
+            d_out = K.grouped_to_heads(g_o.dx.to(out.dtype), ctx.output_ctx.order, kk, b, sl, dh)
         else:
-            dq = _contig16(dqh.view(b, h, kk, sl, dh).permute(0, 3, 2, 1, 4)).view(b * sl * kk, h * dh)
+            d_out = _contig16(g_o.dx.to(out.dtype).view(b, sl, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, sl, dh)
+        dqh, dkh, dvh = torch.autograd.grad(out, (qv, kv, vv), d_out)
+        # the query gradient goes straight from the head layout to grouped rows:
+        # the query projection's backward then reads it by TMA
+        dq = K.heads_to_grouped(dqh.contiguous(), ctx.query_ctx.order, kk)
+        ctx.query_ctx.y_was_grouped = True
         dk = _contig16(dkh.transpose(1, 2)).view(b * sl, h * dh)
         dv = _contig16(dvh.transpose(1, 2)).view(b * sl, h * dh)
     else:

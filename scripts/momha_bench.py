@@ -67,7 +67,7 @@ def main():
             projections()
     kern = {lab: {"ms_per_launch": v["ms_per_launch"], "launches_per_step": v["launches"] / 5}
             for lab, v in lt.summary().items()}
-    ms_layer = timed(layer, steps=5, warmup=2)
+    ms_layer = timed(layer, steps=20, warmup=3)
     flops = 12.0 * t * k * d * dp_
     line = {
         "workload": "C3 MoMHA: B=8 x seq 4096 (T=32768), E=16, k=4, d_model=2048, d_head=128, d_proj=512, causal, bf16",

@@ -118,3 +118,23 @@ def test_momha_c3_full_size_vs_oracle():
     assert all(v <= 2e-2 for v in errs.values()), errs
     # tokens outside the sampled sequence get no gradient
     assert float(gr.dx[:lo].abs().max() if lo else 0.0) == 0.0
+
+
+def test_grouped_to_heads_inverts_heads_to_grouped():
+    """grouped slot rows -> head layout -> grouped rows is the identity (bf16 and fp32)."""
+    for dt in (torch.bfloat16, torch.float32):
+        g = torch.Generator(device="cuda").manual_seed(3)
+        b, seq, k, h, dh, e = 2, 96, 3, 2, 64, 6
+        t = b * seq
+        routing = sm.topk_select(torch.softmax(torch.randn(t, e, device="cuda", generator=g), 1), k)
+        order = sm.compute_grouped_order(routing)
+        rows = torch.randn(t * k, h * dh, device="cuda", generator=g).to(dt)
+        heads = sm.kernels.grouped_to_heads(rows, order, k, b, seq, dh)
+        # head layout (b, h*k, S, dh): head hh*k + j of token (b, s) = grouped row of slot (b*S+s)*k + j
+        slots = rows[order.inverse().long()].view(b, seq, k, h, dh).permute(0, 3, 2, 1, 4).reshape(b, h * k, seq, dh)
+        assert torch.equal(heads, slots)
+        assert torch.equal(sm.kernels.heads_to_grouped(heads, order, k), rows)
+        w = torch.rand(t * k, device="cuda", generator=g)
+        acc = torch.float32 if dt == torch.bfloat16 else torch.float64   # the kernel's accumulate type
+        want = (rows.to(acc) * w[order.o.long()].to(acc)[:, None]).to(dt)
+        assert torch.equal(sm.kernels.scale_grouped_rows(rows, order, w), want)
