@@ -67,8 +67,14 @@ constexpr int G_RSTEP = GATHER_WARPS * 4;   // rows covered by one pass of all g
 // Gather mode: A rows fetched by TMA tile::gather4 from the producer lanes
 // instead of cp.async.  Measured at C1 layer 1 (base clock, tensor-pipe active):
 // 0 rows 72 %, 32 rows 57 % — each gather4 costs far more TMA issue time than
-// the 512 B it moves, so the cp.async warps carry all rows.
-constexpr int TG_ROWS = 0;
+// the 512 B it moves, so the cp.async warps carry all rows.  Round 2 (ncu, no
+// clock lock): 0 rows 5.58 ms / 89.7 % tensor-pipe, 64 rows 9.87 ms / 35.7 %
+// (MMA issuer waiting on operands 78 % of the time).  SMOE_TG_ROWS (a multiple
+// of 16 below 128) rebuilds the split for A/B.
+#ifndef SMOE_TG_ROWS
+#define SMOE_TG_ROWS 0
+#endif
+constexpr int TG_ROWS = SMOE_TG_ROWS;
 constexpr int G_RPT = (128 - TG_ROWS) / G_RSTEP;  // rows per cp.async gather thread per k-block
 constexpr int EPI_COLS = TN / (EPI_WARPS / 4);
 constexpr int STG_BYTES = 32 * 128;        // per-epilogue-warp staging tile: 32 rows x 64 bf16
