@@ -144,10 +144,15 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
 // Slot rows <-> the attention core's head layout.  One warp moves kHeadRows
 // grouped rows per pass: every lane issues its 16-byte loads for all of them
 // before the first store (a row is only h * d_head * 2 B = 1 KB at C3, so one
-// row per warp left the copy latency-bound at ~4.4 TB/s).
+// row per warp left the copy latency-bound at ~4.4 TB/s).  C3 (268 MB moved,
+// scripts/heads_move_bench.py): 2 rows 65 us, 4 rows 53.7, 8 rows 50.4, 16 rows
+// 53; the 16-byte-element torch permute of the same bytes takes 42 us.
 //   TO_HEADS = false: out[i] (grouped row) <- heads[b][hh*k + j][pos][:]
 //   TO_HEADS = true : heads[b][hh*k + j][pos][:] <- grouped[i]
-constexpr int kHeadRows = 4;
+#ifndef SMOE_HEAD_ROWS
+#define SMOE_HEAD_ROWS 8
+#endif
+constexpr int kHeadRows = SMOE_HEAD_ROWS;
 template <typename T, bool TO_HEADS>
 __global__ void __launch_bounds__(kRowThreads) heads_grouped_kernel(const T *__restrict__ src, int64_t seq_len,
                                                                     int k, int h, int dh,
