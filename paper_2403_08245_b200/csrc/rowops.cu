@@ -88,6 +88,10 @@ __global__ void __launch_bounds__(kRowThreads) group_kernel(const T *__restrict_
 // (k times, from DRAM when x exceeds L2); this reads it once.
 // FK > 0: the fan-out is a compile-time constant (1, 2, 4, 8: destinations and
 // weights stay in registers and the k stores of a chunk issue back to back).
+#ifndef SMOE_GROUP_INV_UNROLL
+#define SMOE_GROUP_INV_UNROLL 1
+#endif
+constexpr int kGroupInvUnroll = SMOE_GROUP_INV_UNROLL;   // source chunks in flight per lane (A/B)
 template <typename T, bool VEC, int FK>
 __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restrict__ x, int64_t d,
                                                                 const int32_t *__restrict__ inv, int64_t t_rows,
@@ -112,6 +116,7 @@ __global__ void __launch_bounds__(kRowThreads) group_inv_kernel(const T *__restr
   }
   if (VEC) {
     constexpr int N = Vec<T>::N;
+#pragma unroll kGroupInvUnroll
     for (int64_t c = (int64_t)lane * N; c < d; c += 32 * N) {
       const Vec<T> v = ldv(src + c);
 #pragma unroll
