@@ -331,20 +331,23 @@ def test_fp32_check_mode_accumulates_in_64_bit():
     assert float(dw[0, 0, 0]) == 1.0
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
-def test_grouped_row_reductions_match_slot_order(k):
-    """fanout_reduce / combine over grouped rows (through the inverse
-    permutation) are bit-identical to the slot-ordered kernels."""
+@pytest.mark.parametrize("k,d,dt", [(1, 264, torch.bfloat16), (2, 264, torch.bfloat16), (3, 264, torch.bfloat16),
+                                    (4, 264, torch.bfloat16), (8, 264, torch.bfloat16), (2, 130, torch.bfloat16),
+                                    (4, 96, torch.float32), (3, 33, torch.float64)])
+def test_grouped_row_reductions_match_slot_order(k, d, dt):
+    """fanout_reduce / combine / combine_grad_p over grouped rows (through the
+    inverse permutation) are bit-identical to the slot-ordered kernels
+    (vectorised and scalar paths, bf16 / fp32 / fp64 storage)."""
     g = torch.Generator(device="cuda").manual_seed(k)
-    tokens, e, d = 777, 8, 264
+    tokens, e = 777, 8
     routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
     order = sm.compute_grouped_order(routing)
-    slots = (torch.rand((tokens * k, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    slots = (torch.rand((tokens * k, d), device="cuda", generator=g) * 2 - 1).to(dt)
     grouped = slots[order.o.long()]                     # row i = slot o[i]
     inv = order.inverse()
     assert torch.equal(sm.kernels.fanout_reduce(grouped, k, inverse=inv), sm.kernels.fanout_reduce(slots, k))
     p = routing.p.float()
     assert torch.equal(sm.kernels.combine(p, grouped, inverse=inv), sm.kernels.combine(p, slots))
-    dy = (torch.rand((tokens, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), device="cuda", generator=g) * 2 - 1).to(dt)
     assert torch.equal(sm.kernels.combine_grad_p(dy, grouped, tokens, k, inverse=inv),
                        sm.kernels.combine_grad_p(dy, slots, tokens, k))
