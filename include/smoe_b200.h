@@ -158,6 +158,18 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
  * core's head layout heads[batch][hh * k + j][t % seq_len][0:d_head] for
  * hh = 0 .. heads_per_slot - 1, i.e. out[i] = the slot's d_proj-wide row.  One
  * pass replaces the head->slot permute and the grouped copy of the slot rows. */
+/* scatter2scatter whose output rows go straight into the attention core's
+ * head layout heads[batch][hh * k_slots + j][t % seq_len][0:d_head] (row i's
+ * slot s = order[i], token t = s / k_slots, choice j = s % k_slots; bf16
+ * tcgen05 only).  epilogue SMOE_EPI_NONE, or SMOE_EPI_ACT_GRAD_SCALED with its
+ * act-grad operand aux_grouped read BY GROUPED ROW (row_scale, dp_part as in
+ * smoe_scatter2scatter_scaled).  d_head must be a multiple of 64. */
+int smoe_scatter2scatter_heads(const void *x, int64_t x_rows, const void *w, int32_t num_experts, int64_t w_rows,
+                               int64_t w_cols, const int32_t *order, const int32_t *expert_offsets, int64_t n,
+                               int32_t fan_out, int32_t grouped_in, int32_t transpose_w, int32_t epilogue,
+                               int32_t activation, const float *row_scale, const void *aux_grouped, float *dp_part,
+                               int32_t dp_parts, int64_t seq_len, int32_t k_slots, int32_t d_head, void *heads,
+                               void *stream);
 int smoe_heads_to_grouped(const void *heads, int64_t batch, int64_t seq_len, int32_t k, int32_t heads_per_slot,
                           int32_t d_head, const int32_t *order, int64_t n, int32_t dtype, void *out, void *stream);
 /* the reverse: heads[batch][hh * k + j][t % seq_len][:] = grouped[i][hh * d_head :] for the

@@ -67,6 +67,8 @@ SIGNATURES = {
     "smoe_dp_parts": (_i32, [_i64]),
     "smoe_group_inv": (_c.c_int, [_vp, _i64, _i64, _vp, _i32, _vp, _i32, _vp, _vp]),
     "smoe_heads_to_grouped": (_c.c_int, [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp]),
+    "smoe_scatter2scatter_heads": (_c.c_int, [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
+                                              _i32, _i32, _vp, _vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
     "smoe_grouped_to_heads": (_c.c_int, [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp]),
     "smoe_scale_grouped_rows": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _vp]),
     "smoe_dp_from_partials": (_c.c_int, [_vp, _i64, _i32, _vp, _vp, _vp]),

@@ -51,6 +51,9 @@ int router_gate(const void *, int, const float *, int64_t, int, int, int, int, f
                 cudaStream_t);
 bool tc_available();
 bool tc_supports_s2s(int64_t d_in, int64_t d_out, const void *x, const void *w, const void *out);
+int tc_scatter2scatter_heads(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
+                             const int32_t *, int64_t, int, int, int, int, int, const float *, const void *, float *, int,
+                             int64_t, int, int, void *, cudaStream_t);
 int tc_scatter2scatter(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *, int64_t, int, int, int, int, int, int, void *, void *, const void *, cudaStream_t);
 int tc_group_xty(const void *, const void *, const int32_t *, int, int64_t, int64_t, int64_t, void *, cudaStream_t);
 bool tc_supports_combine(int, int64_t, int64_t, const void *, const void *, const void *);
@@ -154,6 +157,33 @@ int smoe_scatter2scatter(const void *x, int64_t x_rows, const void *w, int32_t n
   }
   return simt_scatter2scatter(x, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out, grouped_in,
                               grouped_out, transpose_w, dtype, epilogue, activation, out, out2, aux, S(stream));
+}
+
+int smoe_scatter2scatter_heads(const void *x, int64_t x_rows, const void *w, int32_t num_experts, int64_t w_rows,
+                               int64_t w_cols, const int32_t *order, const int32_t *expert_offsets, int64_t n,
+                               int32_t fan_out, int32_t grouped_in, int32_t transpose_w, int32_t epilogue,
+                               int32_t activation, const float *row_scale, const void *aux_grouped, float *dp_part,
+                               int32_t dp_parts, int64_t seq_len, int32_t k_slots, int32_t d_head, void *heads,
+                               void *stream) {
+  REQUIRE(epilogue == SMOE_EPI_NONE || epilogue == SMOE_EPI_ACT_GRAD_SCALED, SMOE_EINVAL,
+          "scatter2scatter_heads takes SMOE_EPI_NONE or SMOE_EPI_ACT_GRAD_SCALED");
+  REQUIRE(activation >= SMOE_ACT_GELU && activation <= SMOE_ACT_IDENTITY, SMOE_EINVAL, "bad activation");
+  REQUIRE(fan_out >= 1 && k_slots >= 1 && seq_len >= 1 && d_head >= 1, SMOE_EINVAL, "bad dimensions");
+  REQUIRE(n % ((int64_t)k_slots * seq_len) == 0, SMOE_ESHAPE, "slots must be batch * seq_len * k_slots");
+  if (grouped_in)
+    REQUIRE(x_rows == n, SMOE_ESHAPE, "grouped input rows vs slots");
+  else
+    REQUIRE(x_rows * fan_out == n, SMOE_EINVAL, "scattered input rows * fan_out must equal T*k");
+  const int64_t d_out = transpose_w ? w_rows : w_cols;
+  REQUIRE(!dp_part || dp_parts == smoe_dp_parts(d_out), SMOE_EINVAL, "dp_parts must be smoe_dp_parts(d_out)");
+  if (n == 0) return SMOE_OK;
+  REQUIRE(epilogue != SMOE_EPI_ACT_GRAD_SCALED || (aux_grouped && row_scale), SMOE_EINVAL,
+          "EPI_ACT_GRAD_SCALED needs the grouped act-grad operand and row scales");
+  REQUIRE(x && w && order && expert_offsets && heads, SMOE_EINVAL, "scatter2scatter_heads: null pointer");
+  REQUIRE(tc_available(), SMOE_ENOTSUP, "head-layout output runs on the tcgen05 engine");
+  return tc_scatter2scatter_heads(x, x_rows, w, num_experts, w_rows, w_cols, order, expert_offsets, n, fan_out,
+                                  grouped_in, transpose_w, epilogue, activation, row_scale, aux_grouped, dp_part,
+                                  dp_parts, seq_len, k_slots, d_head, heads, S(stream));
 }
 
 int smoe_group_xty_scattered(const void *x, int64_t x_rows, int32_t x_fan_out, int32_t x_grouped, const void *y,

@@ -640,11 +640,18 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         const bool slab_tma = tma_out && slab0 + 32 <= tl.m_end;
         const int slab_row = (int)(GK ? (int64_t)tl.e * p.M + slab0 : slab0);
         long long dst = -1;
+        const bool heads = !GK && p.hd_dh > 0;
         if (row < tl.m_end) {
-          if (!GK && p.peer_out)  // absolute address of the row in its owner's buffer
+          if (!GK && p.peer_out) {  // absolute address of the row in its owner's buffer
             dst = (long long)(p.peer_out[p.row_src[row]] + (uint64_t)p.row_slot[row] * (uint64_t)p.N * 2u);
-          else
+          } else if (heads) {       // element offset of the slot's head 0 in the head layout
+            const int64_t s = p.order[row];
+            const int64_t t = s / p.hd_k;
+            const int64_t b = t / p.hd_seq;
+            dst = (((b * (p.N / p.hd_dh)) * p.hd_k + (s - t * p.hd_k)) * p.hd_seq + (t - b * p.hd_seq)) * p.hd_dh;
+          } else {
             dst = GK ? (int64_t)tl.e * p.M + row : (p.grouped_out ? row : (int64_t)p.order[row]);
+          }
         }
         long long cdst[8];
   #pragma unroll
@@ -720,7 +727,9 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
             for (int i = 0; i < 8; ++i) {
               const int rl = cr + 4 * i;
               uint4 val = make_uint4(0, 0, 0, 0);
-              if (cdst[i] >= 0 && col_ok) val = __ldg(reinterpret_cast<const uint4 *>(p.aux + cdst[i] * p.N + col0 + cc * 8));
+              // head-layout output: the act-grad operand is read by grouped row
+              const long long arow = heads ? (long long)(slab0 + rl) : cdst[i];
+              if (cdst[i] >= 0 && col_ok) val = __ldg(reinterpret_cast<const uint4 *>(p.aux + arow * p.N + col0 + cc * 8));
               sts128(stg + rl * 128 + ((cc ^ (rl & 7)) << 4), val);
             }
             __syncwarp();
@@ -765,8 +774,16 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
               __syncwarp();
             } else {
               __syncwarp();
-              store_staged_rows(stg, (!GK && p.peer_out) ? nullptr : (pass == 0 ? p.out : p.out2), cdst, col0, col_ok,
-                                p.N, cr, cc);
+              if (heads) {
+                // the 64-column chunk lies in one head: shift the base so that
+                // row offset + col0 + 8 cc lands at head (col0 / dh), column col0 % dh
+                const int64_t hstride = (int64_t)p.hd_k * p.hd_seq * p.hd_dh;
+                __nv_bfloat16 *hb = p.out + ((col0 / p.hd_dh) * hstride + (col0 % p.hd_dh) - col0);
+                store_staged_rows(stg, hb, cdst, col0, col_ok, 1, cr, cc);
+              } else {
+                store_staged_rows(stg, (!GK && p.peer_out) ? nullptr : (pass == 0 ? p.out : p.out2), cdst, col0, col_ok,
+                                  p.N, cr, cc);
+              }
             }
           }
         }
@@ -1243,7 +1260,8 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
                     int epi, int act, void *out, void *out2, const void *aux, const float *pw, float *yacc,
                     int combine_cols, cudaStream_t st, const uint64_t *peer_out = nullptr,
                     const int32_t *row_src = nullptr, const int32_t *row_slot = nullptr,
-                    float *dp_part = nullptr, int dp_parts = 0, const unsigned long long *arrive = nullptr) {
+                    float *dp_part = nullptr, int dp_parts = 0, const unsigned long long *arrive = nullptr,
+                    int64_t hd_seq = 0, int hd_k = 0, int hd_dh = 0) {
   const int64_t d_in = trans ? w_cols : w_rows;
   const int64_t d_out = trans ? w_rows : w_cols;
   CUtensorMap ta, tb;
@@ -1285,6 +1303,9 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
   p.group_m = band_rows(d_in);
   p.timing = getenv("SMOE_TC_TIMING") ? atoi(getenv("SMOE_TC_TIMING")) : 0;
   p.arrive = arrive;
+  p.hd_seq = hd_seq;
+  p.hd_k = hd_k;
+  p.hd_dh = hd_dh;
   const int64_t max_tiles = ((n + TM - 1) / TM + E) * ((d_out + TN - 1) / TN);
   CUtensorMap tc = ta, tc2 = ta;  // unused unless the output is grouped
   if (gout) {
@@ -1292,14 +1313,14 @@ static int s2s_impl(const void *x, int64_t x_rows, const void *w, int E, int64_t
     if (p.out2 && !encode_out_map(&tc2, out2, n, d_out)) return fail(SMOE_ECUDA, "cuTensorMapEncodeTiled(out2) failed");
   }
   if (gin) {
-    if (!peer_out && wide_for(d_in, epi)) {
+    if (!peer_out && !hd_dh && wide_for(d_in, epi)) {
       const int64_t wide_tiles = ((n + 2 * TM - 1) / (2 * TM) + E) * ((d_out + TN - 1) / TN);
       p.group_m = (p.group_m + 1) / 2;  // bands in 512-row blocks
       p.wide_defer = wide_defer();
       if (!trans) return launch<A_ROWS, B_W_MN, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
       return launch<A_ROWS, B_W_K, false, true, true>(ta, tb, tc, tc2, p, wide_tiles, st);
     }
-    if (epi == EPI_COMBINE || peer_out || staged_for(false, gout, d_in)) {
+    if (epi == EPI_COMBINE || peer_out || hd_dh || staged_for(false, gout, d_in)) {
       if (!trans) return launch<A_ROWS, B_W_MN, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
       return launch<A_ROWS, B_W_K, false, true>(ta, tb, tc, tc2, p, max_tiles, st);
     }
@@ -1324,6 +1345,17 @@ int scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int E, 
                            const void *aux, float *dp_part, int dp_parts, cudaStream_t st) {
   return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi, act, out, out2,
                   aux, row_scale, nullptr, 1, st, nullptr, nullptr, nullptr, dp_part, dp_parts);
+}
+
+// Output rows scattered straight into the attention core's head layout
+// (MoMHA): plain or routing-weight-scaled act-grad epilogue (aux by grouped row).
+int scatter2scatter_heads(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                          const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int trans,
+                          int epi, int act, const float *row_scale, const void *aux, float *dp_part, int dp_parts,
+                          int64_t seq_len, int k_slots, int d_head, void *heads, cudaStream_t st) {
+  return s2s_impl(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, 0, trans, epi, act, heads, nullptr,
+                  aux, row_scale, nullptr, 1, st, nullptr, nullptr, nullptr, dp_part, dp_parts, nullptr, seq_len, k_slots,
+                  d_head);
 }
 
 // The scaled epilogues on rows delivered by peers (expert parallelism): grouped

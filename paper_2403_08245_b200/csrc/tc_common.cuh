@@ -61,6 +61,13 @@ struct Params {
   int sync_chunk;   // k-blocks per chunk
   int sync_slack;   // chunks
   int nclusters;
+  // Head-layout output (staged epilogue, grouped-M, hd_dh > 0): out is the
+  // attention core's [batch][h * hd_k][hd_seq][hd_dh] tensor and output row i
+  // (slot s = order[i]: token s / hd_k, choice s % hd_k) is scattered into
+  // its h heads; an act-grad operand (aux) is then read by grouped row.
+  int64_t hd_seq;
+  int hd_k;
+  int hd_dh;
 };
 
 __device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t *p) {

@@ -416,6 +416,9 @@ int scatter2scatter_scaled(const void *, int64_t, const void *, int, int64_t, in
 int scatter2scatter_scaled_gated(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *,
                                  const int32_t *, int64_t, int, int, int, const float *, void *, void *, const void *,
                                  float *, int, const unsigned long long *, cudaStream_t);
+int scatter2scatter_heads(const void *, int64_t, const void *, int, int64_t, int64_t, const int32_t *, const int32_t *,
+                          int64_t, int, int, int, int, int, const float *, const void *, float *, int, int64_t, int, int,
+                          void *, cudaStream_t);
 }  // namespace tc2
 bool tc2_supports_experts(int E);  // the CTA-pair kernel's smem holds a per-expert tile table
 
@@ -526,6 +529,19 @@ int tc_scatter2scatter_scaled(const void *x, int64_t x_rows, const void *w, int 
     return fail(SMOE_ENOTSUP, "scaled epilogues need the CTA-pair engine, d_in, d_out multiples of 8");
   return tc2::scatter2scatter_scaled(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, gout, trans, epi,
                                      act, row_scale, out, out2, aux, dp_part, dp_parts, st);
+}
+
+int tc_scatter2scatter_heads(const void *x, int64_t x_rows, const void *w, int E, int64_t w_rows, int64_t w_cols,
+                             const int32_t *order, const int32_t *offsets, int64_t n, int fan_out, int gin, int trans,
+                             int epi, int act, const float *row_scale, const void *aux, float *dp_part, int dp_parts,
+                             int64_t seq_len, int k_slots, int d_head, void *heads, cudaStream_t st) {
+  const int64_t d_in = trans ? w_cols : w_rows, d_out = trans ? w_rows : w_cols;
+  if (!(tc_ctas() == 2 && E <= 1024 && tc2_supports_experts(E) && tc_supports_s2s(d_in, d_out, x, w, heads)))
+    return fail(SMOE_ENOTSUP, "head-layout output needs the CTA-pair engine, d_in, d_out multiples of 8");
+  if (d_head % 64 || d_out % d_head)
+    return fail(SMOE_ENOTSUP, "head-layout output needs d_head a multiple of 64 dividing d_out");
+  return tc2::scatter2scatter_heads(x, x_rows, w, E, w_rows, w_cols, order, offsets, n, fan_out, gin, trans, epi, act,
+                                    row_scale, aux, dp_part, dp_parts, seq_len, k_slots, d_head, heads, st);
 }
 
 // group_xty with scattered (gathered) operands: CTA-pair kernels only.

@@ -463,6 +463,66 @@ def heads_to_grouped(heads: torch.Tensor, order: GroupedOrder, k: int) -> torch.
     return out
 
 
+def scatter2scatter_heads(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    order: GroupedOrder,
+    fan_out: int,
+    grouped_in: bool,
+    *,
+    batch: int,
+    seq_len: int,
+    k: int,
+    d_head: int,
+    transpose_w: bool = False,
+    row_scale: torch.Tensor | None = None,
+    act_grad_of: torch.Tensor | None = None,
+    dp_partials: torch.Tensor | None = None,
+) -> torch.Tensor:
+    """scatter2scatter whose output goes straight into the attention core's head
+    layout (batch, h*k, seq_len, d_head): output row i (slot order.o[i]) lands in
+    heads hh*k + j of its token (bf16, tcgen05; d_head a multiple of 64).
+
+    act_grad_of given (GROUPED rows, [n, d_out]): the routing-weight-scaled
+    identity act-grad epilogue of parallel_linear's dp-in-epilogue backward —
+    out = row_scale[o[i]] * (x @ W) and, with dp_partials, the partial dot
+    products with act_grad_of's row i.
+    """
+    if x.dtype != torch.bfloat16:
+        raise ValueError("head-layout output runs on the bf16 tensor-core engine")
+    num_slots = order.num_slots
+    d_in = w.shape[2] if transpose_w else w.shape[1]
+    d_out = w.shape[1] if transpose_w else w.shape[2]
+    require_dims(x.shape[1] == d_in, "input width vs expert weights", tuple(x.shape), (d_in, d_out))
+    require_dims(num_slots == batch * seq_len * k, "slots vs batch*seq_len*k", (num_slots,), (batch * seq_len * k,))
+    if d_out % d_head:
+        raise ValueError(f"output width {d_out} is not divisible by d_head {d_head}")
+    x, w = _cuda(x, "x"), _cuda(w, "w")
+    heads = torch.empty((batch, (d_out // d_head) * k, seq_len, d_head), dtype=x.dtype, device=x.device)
+    epi, scale_ptr, aux_ptr, parts, parts_ptr = _lib.EPI_NONE, None, None, 0, None
+    if act_grad_of is not None:
+        require_dims(tuple(act_grad_of.shape) == (num_slots, d_out), "act-grad operand", tuple(act_grad_of.shape),
+                     (num_slots, d_out))
+        scale = _cuda(row_scale.to(torch.float32), "row_scale").contiguous()
+        aux = _cuda(act_grad_of, "act_grad_of").contiguous()
+        epi, scale_ptr, aux_ptr = _lib.EPI_ACT_GRAD_SCALED, scale.data_ptr(), aux.data_ptr()
+        if dp_partials is not None:
+            parts = _lib.load().smoe_dp_parts(d_out)
+            require_dims(tuple(dp_partials.shape) == (num_slots, parts), "dp partials", tuple(dp_partials.shape),
+                         (num_slots, parts))
+            parts_ptr = dp_partials.data_ptr()
+    t0 = _lt.begin()
+    st = _lib.load().smoe_scatter2scatter_heads(
+        x.data_ptr(), x.shape[0], w.data_ptr(), w.shape[0], w.shape[1], w.shape[2], order.o.data_ptr(),
+        order.bin_offsets.data_ptr(), num_slots, fan_out, int(grouped_in), int(transpose_w), epi,
+        _lib.ACT_IDENTITY if act_grad_of is not None else 0, scale_ptr, aux_ptr, parts_ptr, parts, seq_len, k,
+        d_head, heads.data_ptr(), _stream(x))
+    _lt.end("scatter2scatter " + ("G" if grouped_in else "S") + "->heads" + (" W^T" if transpose_w else ""), t0)
+    _lib.check(st, "scatter2scatter_heads")
+    _credit(order, d_in, d_out)
+    return heads
+
+
 def grouped_to_heads(grouped: torch.Tensor, order: GroupedOrder, k: int, batch: int, seq_len: int,
                      d_head: int) -> torch.Tensor:
     """The attention core's head layout (batch, h*k, seq_len, d_head) from grouped

@@ -396,6 +396,9 @@ _GQA = os.environ.get("SMOE_MOMHA_GQA", "1") != "0"
 
 # SMOE_MOMHA_GROUPED=0: slot rows in slot order around the attention core (A/B)
 _MOMHA_GROUPED = os.environ.get("SMOE_MOMHA_GROUPED", "1") != "0"
+# SMOE_MOMHA_HEADS_OUT=0: the q projection and the attention-output gradient
+# leave their GEMMs as grouped rows and move to the head layout separately (A/B)
+_MOMHA_HEADS_OUT = os.environ.get("SMOE_MOMHA_HEADS_OUT", "1") != "0"
 
 
 def _contig16(t: torch.Tensor) -> torch.Tensor:
@@ -519,17 +522,27 @@ def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: Group
     # pass moves them into the core's head layout, one pass brings the core's
     # output back as grouped rows, and the output projection then reads them by
     # TMA (no row gather) and its backward stays in grouped order too
-    q_layout = SCATTERED_TO_GROUPED if grouped else SCATTERED_TO_SCATTERED
-    q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=q_layout,
-                              tile=tile, training=training, ledger=ledger, name="momha.query")
+    heads_out = grouped and config.d_head % 64 == 0 and _MOMHA_HEADS_OUT
+    if heads_out:
+        # the query projection writes the attention core's head layout directly
+        b_, kk_, dh_ = n // seq_len, config.k, config.d_head
+        q = K.scatter2scatter_heads(x, weights.wq, order, kk_, False, batch=b_, seq_len=seq_len, k=kk_, d_head=dh_)
+        query_ctx = pl.LinearContext(x=x, w=weights.wq, order=order, p=None, fan_out=kk_, x_was_grouped=False,
+                                     y_was_grouped=True, y_hat=None)
+    else:
+        q_layout = SCATTERED_TO_GROUPED if grouped else SCATTERED_TO_SCATTERED
+        q, query_ctx = pl.forward(x, weights.wq, order, p=None, fan_out=config.k, layout=q_layout,
+                                  tile=tile, training=training, ledger=ledger, name="momha.query")
     attn_graph = None
     o_layout = SCATTERED_TO_SCATTERED
     if fused:
         # keep the attention core's autograd graph for the backward instead of
         # recomputing it (attention_backward, the reference's :330-377 form)
         kk, dh = config.k, config.d_head
-        b, h = n // seq_len, q.shape[1] // dh
-        if grouped:
+        b, h = n // seq_len, weights.wq.shape[2] // dh
+        if heads_out:
+            qh = q
+        elif grouped:
             qh = K.grouped_to_heads(q, order, kk, b, seq_len, dh)
         else:   # slot rows (b, S, k, h, d) -> heads (b, h*k, S, d) by 16-byte-element copies
             qh = _contig16(q.view(b, seq_len, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, seq_len, dh)
@@ -559,11 +572,18 @@ def momha_forward(x, weights: MomhaWeights, routing: RoutingResult, order: Group
 
 def momha_backward(ctx: MomhaContext, dy, *, tile: TileConfig | None = None, ledger=None) -> MomhaGradients:
     """Gradients for routed attention; stops at dp (moe_layers.py:460-482)."""
-    g_o = pl.backward(ctx.output_ctx, dy, tile=tile, ledger=ledger, name="momha.output")
+    dx_heads = None
+    if ctx.attn_graph is not None and ctx.output_ctx.x_was_grouped and _MOMHA_HEADS_OUT:
+        _, _, _, _, (b, sl, kk, h, dh) = ctx.attn_graph
+        if dh % 64 == 0:
+            dx_heads = (b, sl, kk, dh)
+    g_o = pl.backward(ctx.output_ctx, dy, tile=tile, ledger=ledger, name="momha.output", dx_heads=dx_heads)
     if ctx.attn_graph is not None:
         qv, kv, vv, out, (b, sl, kk, h, dh) = ctx.attn_graph
         ctx.attn_graph = None
-        if ctx.output_ctx.x_was_grouped:   # the output projection's input gradient comes back as grouped rows
+        if dx_heads is not None:           # the input-gradient GEMM wrote the core's head layout
+            d_out = g_o.dx
+        elif ctx.output_ctx.x_was_grouped:   # the output projection's input gradient comes back as grouped rows
             d_out = K.grouped_to_heads(g_o.dx.to(out.dtype), ctx.output_ctx.order, kk, b, sl, dh)
         else:
             d_out = _contig16(g_o.dx.to(out.dtype).view(b, sl, kk, h, dh).permute(0, 3, 2, 1, 4)).view(b, h * kk, sl, dh)

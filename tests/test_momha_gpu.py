@@ -138,3 +138,33 @@ def test_grouped_to_heads_inverts_heads_to_grouped():
         acc = torch.float32 if dt == torch.bfloat16 else torch.float64   # the kernel's accumulate type
         want = (rows.to(acc) * w[order.o.long()].to(acc)[:, None]).to(dt)
         assert torch.equal(sm.kernels.scale_grouped_rows(rows, order, w), want)
+
+
+def test_scatter2scatter_heads_matches_grouped_gemm_then_move():
+    """The head-layout GEMM output (plain and the scaled act-grad + dp epilogue)
+    equals the grouped-output GEMM followed by grouped_to_heads, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    b, seq, k, e, d_in, dh, hpe = 2, 192, 4, 8, 256, 128, 2
+    d_out = dh * hpe
+    t_ = b * seq
+    routing = sm.topk_select(torch.softmax(torch.randn(t_, e, device="cuda", generator=g), 1), k)
+    order = sm.compute_grouped_order(routing)
+    x = (torch.rand((t_, d_in), device="cuda", generator=g) * 2 - 1).bfloat16()
+    w = ((torch.rand((e, d_in, d_out), device="cuda", generator=g) * 2 - 1) / 16).bfloat16()
+    heads = sm.kernels.scatter2scatter_heads(x, w, order, k, False, batch=b, seq_len=seq, k=k, d_head=dh)
+    ref = sm.kernels.grouped_to_heads(sm.scatter2scatter(x, w, order, k, sm.SCATTERED_TO_GROUPED), order, k, b, seq, dh)
+    assert torch.equal(heads, ref)
+    # transposed weights, grouped input, scaled identity act-grad with dp partials
+    dyg = (torch.rand((t_ * k, d_out), device="cuda", generator=g) * 2 - 1).bfloat16()
+    xg = (torch.rand((t_ * k, d_in), device="cuda", generator=g) * 2 - 1).bfloat16()
+    wt = ((torch.rand((e, d_in, d_out), device="cuda", generator=g) * 2 - 1) / 16).bfloat16()
+    p_flat = routing.p.reshape(-1).float().contiguous()
+    parts_h = torch.empty((t_ * k, sm.kernels.dp_parts(d_in)), device="cuda")
+    parts_g = torch.empty_like(parts_h)
+    hx = sm.kernels.scatter2scatter_heads(dyg, wt, order, 1, True, batch=b, seq_len=seq, k=k, d_head=dh // 2,
+                                          transpose_w=True, row_scale=p_flat, act_grad_of=xg, dp_partials=parts_h)
+    gx = sm.kernels.scatter2scatter_scaled(dyg, wt, order, 1, sm.GROUPED_TO_GROUPED, row_scale=p_flat,
+                                           activation="identity", out=torch.empty_like(xg), act_grad_of=xg,
+                                           dp_partials=parts_g, transpose_w=True)
+    assert torch.equal(hx, sm.kernels.grouped_to_heads(gx, order, k, b, seq, dh // 2))
+    assert torch.equal(parts_h, parts_g)
