@@ -523,8 +523,13 @@ static int launch_onepass(const int64_t *ids, int64_t n, int E, int32_t *hist, s
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  const cudaError_t e =
+      cudaLaunchKernelEx(&lc, kern, ids, n, E, chunk, hist, sorted_scattered, sorted_expert, inverse, offsets);
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+    (void)cudaGetLastError();   // no co-resident grid here (e.g. a partitioned device): two-pass path
+    return 0;
+  }
   *used = true;
-  cudaLaunchKernelEx(&lc, kern, ids, n, E, chunk, hist, sorted_scattered, sorted_expert, inverse, offsets);
   return check_launch("route_sort(one-pass)", 1);
 }
 
