@@ -148,6 +148,14 @@ _SCALED = os.environ.get("SMOE_MLP_SCALED", "1") != "0"
 # staged scattered-row epilogue is not what limits those GEMMs; off.
 _GROUPED_REDUCE = os.environ.get("SMOE_GROUPED_REDUCE", "0") == "1"
 
+# SMOE_L1_GROUPED=1: the scaled forward copies X into grouped order (into the
+# layer-2 output's storage, so no extra buffer) and runs layer 1 as a TMA-fed
+# grouped-input GEMM instead of gathering X's rows inside the GEMM.  Layer 1
+# drops 6.25 -> 5.77 ms (C1) and 3.25 -> 2.94 ms (C2), but under the power cap
+# the other GEMMs slow by about as much and the copy is one more pass: C1
+# 912-915 k vs 909-914 k tok/s, C2 1.588-1.591 M vs 1.594-1.601 M; off.
+_L1_GROUPED = os.environ.get("SMOE_L1_GROUPED", "0") == "1"
+
 
 def set_scaled(enabled: bool) -> bool:
     """Select the routing-weight-scaled MLP path (True) or the literal one; returns the previous value."""
@@ -197,15 +205,23 @@ def smoe_mlp_forward(
         p_flat = routing.p.reshape(-1).to(torch.float32).contiguous()
         h_pre = torch.empty((n, de), dtype=x.dtype, device=x.device)
         hp = torch.empty((n, de), dtype=x.dtype, device=x.device)
-        K.scatter2scatter_scaled(x, w1, order, k, SCATTERED_TO_GROUPED, row_scale=p_flat, activation=activation,
-                                 out=h_pre, act_out=hp)
+        y_hat_p = torch.empty((n, w2.shape[2]), dtype=x.dtype, device=x.device)
+        if _L1_GROUPED and w2.shape[2] == x.shape[1]:
+            # grouped X staged in the layer-2 output's storage (dead until layer 2
+            # writes it): layer 1 runs TMA-fed instead of gathering rows
+            xg = K.group(x, order, fan_out=k, out=y_hat_p)
+            K.scatter2scatter_scaled(xg, w1, order, 1, GROUPED_TO_GROUPED, row_scale=p_flat,
+                                     activation=activation, out=h_pre, act_out=hp)
+        else:
+            K.scatter2scatter_scaled(x, w1, order, k, SCATTERED_TO_GROUPED, row_scale=p_flat,
+                                     activation=activation, out=h_pre, act_out=hp)
         if _GROUPED_REDUCE:
             # layer 2 writes grouped rows (whole 32-row slabs leave by TMA) and the
             # k-sum gathers each token's rows through the inverse permutation
-            y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_GROUPED)
+            K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_GROUPED, out=y_hat_p)
             y = K.fanout_reduce(y_hat_p, k, inverse=order.inverse())
         else:
-            y_hat_p = K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_SCATTERED)
+            K.scatter2scatter(hp, w2, order, 1, GROUPED_TO_SCATTERED, out=y_hat_p)
             y = K.fanout_reduce(y_hat_p, k)
         if ledger:
             ledger.alloc("mlp.hidden.y", n, de, "forward")

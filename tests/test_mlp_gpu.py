@@ -365,3 +365,30 @@ def test_on_dx_hook_fires_before_dw1_with_final_dx():
     gr2 = sm.smoe_mlp_backward(ctx2, dy)
     for a, b in ((gr.dx, gr2.dx), (gr.dw1, gr2.dw1), (gr.dw2, gr2.dw2), (gr.dp, gr2.dp)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("tokens,e", [(1000, 6), (3, 4)])
+def test_grouped_layer1_forward_bit_identical(tokens, e):
+    """SMOE_L1_GROUPED: layer 1 fed by a grouped copy of X (TMA) instead of the
+    in-GEMM row gather — same K order per output element, so bit-identical."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    d, de, k = 136, 264, 2
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / de ** 0.5).to(torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+    order = sm.compute_grouped_order(routing)
+    out = {}
+    prev = sm.moe_layers._L1_GROUPED
+    try:
+        for grouped in (False, True):
+            sm.moe_layers._L1_GROUPED = grouped
+            y, ctx = sm.smoe_mlp_forward(x, w1, w2, routing, order)
+            assert ctx.scaled is not None
+            gr = sm.smoe_mlp_backward(ctx, dy)
+            out[grouped] = (y, ctx.h_pre, gr.dx, gr.dw1, gr.dw2, gr.dp)
+    finally:
+        sm.moe_layers._L1_GROUPED = prev
+    for name, a, b in zip(("y", "h_pre", "dx", "dw1", "dw2", "dp"), out[False], out[True]):
+        assert torch.equal(a, b), name
