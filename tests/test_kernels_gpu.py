@@ -351,3 +351,44 @@ def test_grouped_row_reductions_match_slot_order(k, d, dt):
     dy = (torch.rand((tokens, d), device="cuda", generator=g) * 2 - 1).to(dt)
     assert torch.equal(sm.kernels.combine_grad_p(dy, grouped, tokens, k, inverse=inv),
                        sm.kernels.combine_grad_p(dy, slots, tokens, k))
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    e = int(rng.choice([1, 2, 3, 7, 8, 16, 33, 64, 128]))
+    k = int(rng.integers(1, min(e, 8) + 1))
+    tokens = int(rng.choice([1, 2, 5, 31, 129, 257, 700, 1500]))
+    d_in = int(8 * rng.integers(1, 70))
+    d_out = int(8 * rng.integers(1, 70))
+    d_in = 8 if seed in (3, 10) else d_in      # one 8-wide k-block
+    d_out = 8 if seed in (7, 16) else d_out    # one 8-wide output column block
+    return rng, tokens, k, e, d_in, d_out
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_bf16_random_shapes_vs_oracle(seed):
+    """Seeded random sweep over expert counts (1..128), fan-out (1..8), token
+    counts down to one and widths down to 8 (sub-tile K and N, ragged bins):
+    every layout and transpose flag, plus group_xty, against the oracle."""
+    rng, tokens, k, e, d_in, d_out = _random_case(seed)
+    lname = list(LAYOUTS)[seed % 4]
+    layout, transpose = LAYOUTS[lname], bool((seed // 4) % 2)
+    flavor = ["gate", "all_to_one", "skip_one"][seed % 3]
+    if flavor == "skip_one" and k >= e:
+        flavor = "gate"
+    idx, x, w, fan_out = _problem(rng, tokens, k, e, d_in, d_out, layout, transpose, flavor)
+    xb, wb = bf16_round(x), bf16_round(w)
+    o, off = orc.compute_grouped_order(idx, e)
+    want = orc.scatter2scatter(xb, wb, o, off, fan_out, layout.grouped_in, layout.grouped_out, transpose)
+    order = order_of(idx, e)
+    y = sm.scatter2scatter(t(xb, torch.bfloat16), t(wb, torch.bfloat16), order, fan_out, layout,
+                           transpose_w=transpose)
+    assert rel_err(y, want) <= 2e-2, (lname, transpose, tokens, k, e, d_in, d_out)
+    xg = bf16_round(rng.uniform(-1, 1, (tokens * k, d_in)).astype(np.float32))
+    yg = bf16_round(rng.uniform(-1, 1, (tokens * k, d_out)).astype(np.float32))
+    dw = sm.group_xty(t(xg, torch.bfloat16), t(yg, torch.bfloat16), order)
+    want_dw = orc.group_xty(xg, yg, off)
+    assert rel_err(dw, want_dw) <= 2e-2, ("xty", tokens, k, e, d_in, d_out)
+    counts = np.diff(off)
+    for ex in np.flatnonzero(counts == 0):
+        assert float(dw[ex].float().abs().max()) == 0.0

@@ -392,3 +392,37 @@ def test_grouped_layer1_forward_bit_identical(tokens, e):
         sm.moe_layers._L1_GROUPED = prev
     for name, a, b in zip(("y", "h_pre", "dx", "dw1", "dw2", "dp"), out[False], out[True]):
         assert torch.equal(a, b), name
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_scaled_mlp_random_shapes_vs_oracle(seed):
+    """Seeded random sweep of the bf16 training path (routing-weight-scaled form,
+    dp from the dH epilogue): expert counts 1..128, fan-out 1..8, widths from 8,
+    one-token batches, all three activations — Y, dX, dW1, dW2, dp vs the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    e = int(rng.choice([1, 2, 5, 8, 16, 40, 128]))
+    k = int(rng.integers(1, min(e, 8) + 1))
+    tokens = int(rng.choice([1, 3, 64, 257, 900]))
+    d = 8 if seed == 4 else int(8 * rng.integers(1, 40))
+    de = 8 if seed == 7 else int(8 * rng.integers(1, 60))
+    act = ["gelu", "silu", "relu"][seed % 3]
+    x = bf16_round(rng.uniform(-1, 1, (tokens, d)).astype(np.float32))
+    w1 = bf16_round((rng.uniform(-1, 1, (e, d, de)) / np.sqrt(d)).astype(np.float32))
+    w2 = bf16_round((rng.uniform(-1, 1, (e, de, d)) / np.sqrt(de)).astype(np.float32))
+    dy = bf16_round(rng.uniform(-1, 1, (tokens, d)).astype(np.float32))
+    idx = np.stack([rng.permutation(e)[:k] for _ in range(tokens)])
+    p = rng.uniform(0.05, 1.0, (tokens, k)).astype(np.float32)
+    p /= p.sum(1, keepdims=True)
+    want_y, st = orc.smoe_mlp_forward(x, w1, w2, idx, p, e, activation=act)
+    want = orc.smoe_mlp_backward(x, w1, w2, p, st, dy, activation=act)
+    y, ctx = _run(x, w1, w2, idx, p, e, act, torch.bfloat16)
+    assert ctx.scaled is not None
+    gr = sm.smoe_mlp_backward(ctx, t(dy, torch.bfloat16))
+    case = (tokens, d, de, e, k, act)
+    assert rel_err(y, want_y) <= 2e-2, case
+    for got, w_, name in zip((gr.dx, gr.dw1, gr.dw2), want[:3], ("dx", "dw1", "dw2")):
+        assert rel_err(got, w_) <= 2e-2, (name, rel_err(got, w_), case)
+    # dp: each entry one dot product, bounded by its absolute dot product
+    absdot = (np.abs(dy).astype(np.float64)[:, None, :] * np.abs(st["y_hat"]).reshape(tokens, k, d)).sum(-1)
+    err = np.abs(np_of(gr.dp).astype(np.float64) - want[3])
+    assert np.all(err <= 2e-2 * absdot + 1e-6), (float((err / np.maximum(absdot, 1e-30)).max()), case)
