@@ -136,3 +136,51 @@ def test_dp_epilogue_backward_bf16(shape, monkeypatch):
             assert rel_err(val, ref) <= 2e-2, (mode, name, rel_err(val, ref))
         assert float(gr.dw[e - 1].float().abs().max()) == 0.0
     assert rel_err(got[True].dp, np_of(got[False].dp)) <= 1e-2
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_bf16_random_shapes_vs_oracle(seed, monkeypatch):
+    """Seeded random sweep of ParallelLinear forward + backward in bf16: every
+    layout, with and without combine weights, fan-out 1 or k on scattered
+    inputs, and the grouped-Y_hat / dp-epilogue flows on and off, against the
+    oracle (f64 on the bf16-rounded inputs) at the bf16 bar."""
+    import sys
+    from oracle import scattermlp_oracle as orc
+    from gpu_util import bf16_round
+    plmod = sys.modules["paper_2403_08245_b200.parallel_linear"]
+    rng = np.random.default_rng(3000 + seed)
+    e = int(rng.choice([1, 3, 8, 16, 64]))
+    k = int(rng.integers(1, min(e, 4) + 1))
+    tokens = int(rng.choice([1, 7, 130, 600]))
+    d_in, d_out = int(8 * rng.integers(1, 50)), int(8 * rng.integers(1, 50))
+    layout = list(LAYOUTS.values())[seed % 4]
+    with_p = bool((seed // 4) % 2)
+    if with_p:      # combine weights need scattered kernel output (parallel_linear.py:118-119)
+        layout = sm.GROUPED_TO_SCATTERED if layout.grouped_in else sm.SCATTERED_TO_SCATTERED
+    fan = 1 if layout.grouped_in else int(rng.choice([1, k]))
+    monkeypatch.setattr(plmod, "_GROUPED_YHAT", bool(seed % 3))
+    monkeypatch.setattr(plmod, "_DP_EPILOGUE", bool(seed % 5))
+    idx = np.stack([rng.permutation(e)[:k] for _ in range(tokens)])
+    n = tokens * k
+    x = bf16_round(rng.uniform(-1, 1, (n if (layout.grouped_in or fan == 1) else n // fan, d_in)))
+    w = bf16_round(rng.uniform(-1, 1, (e, d_in, d_out)) / np.sqrt(d_in))
+    p = rng.uniform(0.05, 1.0, (tokens, k)).astype(np.float32) if with_p else None
+    dy = bf16_round(rng.uniform(-1, 1, ((tokens if with_p else n), d_out)))
+    o, off = orc.compute_grouped_order(idx, e)
+    p64 = None if p is None else p.astype(np.float64)
+    want_y, y_hat = orc.pl_forward(x.astype(np.float64), w.astype(np.float64), o, off, p64, fan,
+                                   layout.grouped_in, layout.grouped_out)
+    want = orc.pl_backward(x.astype(np.float64), w.astype(np.float64), o, off, p64, fan, layout.grouped_in,
+                           layout.grouped_out and not with_p, y_hat, dy.astype(np.float64))
+    order = order_of(idx, e)
+    y, ctx = sm.parallel_linear_forward(t(x, torch.bfloat16), t(w, torch.bfloat16), order,
+                                        p=None if p is None else t(p), fan_out=fan, layout=layout)
+    gr = sm.parallel_linear_backward(ctx, t(dy, torch.bfloat16))
+    case = (tokens, k, e, d_in, d_out, layout, with_p, fan)
+    assert rel_err(y, want_y) <= 2e-2, case
+    assert rel_err(gr.dx, want[0]) <= 2e-2, ("dx", case)
+    assert rel_err(gr.dw, want[1]) <= 2e-2, ("dw", case)
+    if with_p:
+        absdot = (np.abs(dy).astype(np.float64)[:, None, :] * np.abs(y_hat).reshape(tokens, k, d_out)).sum(-1)
+        err = np.abs(np_of(gr.dp).astype(np.float64) - want[2])
+        assert np.all(err <= 2e-2 * absdot + 1e-6), ("dp", case)
