@@ -168,3 +168,43 @@ def test_scatter2scatter_heads_matches_grouped_gemm_then_move():
                                            dp_partials=parts_g, transpose_w=True)
     assert torch.equal(hx, sm.kernels.grouped_to_heads(gx, order, k, b, seq, dh // 2))
     assert torch.equal(parts_h, parts_g)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_momha_bf16_random_shapes_vs_oracle(seed):
+    """Seeded random sweep of the bf16 MoMHA layer (head-layout q projection when
+    d_head % 64 == 0, grouped slot rows otherwise; causal and not): batches of
+    1-3 sequences of 1-96 tokens, k 1-4, d_head 8-128, against the oracle on the
+    same bf16-rounded inputs (Y, dX, dp and all four weight gradients)."""
+    from oracle import scattermlp_oracle as orc
+
+    rng = np.random.default_rng(4000 + seed)
+    k = int(rng.integers(1, 5))
+    hpe = int(rng.choice([1, 2]))
+    d_head = int(rng.choice([8, 32, 64, 128]))
+    e = int(rng.integers(k, 17))
+    d_model = int(8 * rng.integers(2, 33))
+    b, seq = int(rng.integers(1, 4)), int(rng.choice([1, 17, 64, 96]))
+    causal = bool(seed % 2 == 0)
+    cfg = sm.MomhaConfig(d_model=d_model, d_head=d_head, num_heads=k * hpe, heads_per_expert=hpe,
+                         num_experts=e, k=k, causal=causal)
+    wts = sm.init_momha_weights(cfg, seed, dtype=torch.bfloat16)
+    n = b * seq
+    x = t(rng.uniform(-1, 1, (n, d_model)).astype(np.float32), torch.bfloat16)
+    dy = t(rng.uniform(-1, 1, (n, d_model)).astype(np.float32), torch.bfloat16)
+    idx = np.stack([rng.permutation(e)[:k] for _ in range(n)])
+    p = rng.uniform(0.05, 1.0, (n, k)).astype(np.float32)
+    p /= p.sum(1, keepdims=True)
+    routing, order = routing_of(idx, p, e), order_of(idx, e)
+    y, ctx = sm.momha_forward(x, wts, routing, order, cfg, seq)
+    gr = sm.momha_backward(ctx, dy)
+    wq, wk, wv, wo = (np_of(getattr(wts, f)) for f in ("wq", "wk", "wv", "wo"))
+    want_y, st = orc.momha_forward(np_of(x), wq, wk, wv, wo, idx, p, e, seq, d_head, causal)
+    want = orc.momha_backward(np_of(x), wq, wk, wv, wo, p, st, np_of(dy))
+    case = (b, seq, k, hpe, d_head, e, d_model, causal)
+    assert rel_err(y, want_y) <= 2e-2, case
+    for j, name in enumerate(("dx", "dwq", "dwk", "dwv", "dwo")):
+        assert rel_err(getattr(gr, name), want[j]) <= 2e-2, (name, rel_err(getattr(gr, name), want[j]), case)
+    absdot = (np.abs(np_of(dy)).astype(np.float64)[:, None, :] * np.abs(st["y_hat"]).reshape(n, k, d_model)).sum(-1)
+    err = np.abs(np_of(gr.dp).astype(np.float64) - want[5])
+    assert np.all(err <= 2e-2 * absdot + 1e-6), ("dp", case)
