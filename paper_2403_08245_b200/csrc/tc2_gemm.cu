@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
       for (int kb = 0; kb < tl.nkb; ++kb) {
         const uint32_t fb = smem_u32(&lfull_bar[stage]);
         const uint32_t sa = smem_u32(tiles_smem + stage * SBYTES);
-        const int kk = kb * BK;
+        const int kk = kpos(tl, kb) * BK;
         // all lanes wait (keeps the warp converged, so coordinates and
         // addresses stay in uniform registers); one elected lane issues
         if (lockstep && kb % p.sync_chunk == 0) lockstep_gate();
@@ -414,8 +414,8 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           if (p.timing) c_lfull += clock64() - c1;
           uint8_t *sa_ptr = tiles_smem + stage * SBYTES;
           int nk = BK / 16;
-          if (GK && kb == tl.nkb - 1) {
-            const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+          if (GK && kpos(tl, kb) == tl.nkb - 1) {
+            const int valid = (int)(tl.k_len - (int64_t)kpos(tl, kb) * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
               if (valid < 16 * nk) zero_k_rows(sa_ptr, BOXES, valid, 16 * nk, lane);
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         }
         int sg = st0;
         for (int kb = kb0; kb < kb1; ++kb) {
-          const int nk = (GK && kb == tl.nkb - 1) ? nk_last : BK / 16;
+          const int nk = (GK && kpos(tl, kb) == tl.nkb - 1) ? nk_last : BK / 16;
           const uint32_t sa = smem_u32(tiles_smem + sg * SBYTES), sb = sa + ABYTES;
           if (elect_one_sync()) {
 #pragma unroll
@@ -505,11 +505,11 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
           if (p.timing) c_lfull += clock64() - c1;
           uint8_t *sa_ptr = tiles_smem + stage * SBYTES;
           int nk = BK / 16;  // K16 steps issued for this stage
-          if (GK && kb == tl.nkb - 1) {
+          if (GK && kpos(tl, kb) == tl.nkb - 1) {
             // bin tail: rows past the expert's bin belong to the next expert.
             // K16 steps wholly past the bin are skipped; the rest of the last
             // partial step is zeroed by each CTA in its own tiles.
-            const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+            const int valid = (int)(tl.k_len - (int64_t)kpos(tl, kb) * BK);
             if (valid < BK) {
               nk = (valid + 15) / 16;
               // TMA-fed operands only (a gathered operand's copies zero-fill past the bin)
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kernel_threads(AM, BMODE), 1) __cluster_dims__
         if (t < 0) break;
         const Tile tl = decode_tile<GK, TMT, TN>(t, p, s_start, s_off, nN, mM);
         for (int kb = 0; kb < tl.nkb; ++kb) {
-          const int valid = (int)(tl.k_len - (int64_t)kb * BK);
+          const int valid = (int)(tl.k_len - (int64_t)kpos(tl, kb) * BK);
           if (valid < BK) {
             mbar_wait(smem_u32(&lfull_bar[stage]), (parity_bits >> stage) & 1u);
             parity_bits ^= 1u << stage;
@@ -1118,6 +1118,24 @@ static void set_lockstep(Params &q, int clusters, bool eligible) {
   q.nclusters = clusters;
 }
 
+// Serpentine K order (SMOE_TC_SERP: 0 off, 1 wide TMA-fed kernels, 2 every
+// TMA-fed kernel, 3 every TMA-fed kernel by global tile id / grid pairs): a
+// tile streams its k-blocks in reverse when its index within its expert, / 74
+// (the CTA pairs), is odd, so each wave of concurrent tiles starts on the K
+// range the previous wave read last (still in L2).  A tile's accumulation
+// order then depends on its tile shape and place in the schedule.  Measured
+// (profiles/r2_lockstep.txt): dW GEMM -1 %, step +0.2 % (mode 2) to +0.5-1.1 %
+// (mode 3), at the cost of the bit-identity between the expert-parallel and
+// single-GPU paths (and, mode 3, with the grid size) — off by default.
+static void set_serp(Params &q, bool tma_fed, bool wide) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char *env = getenv("SMOE_TC_SERP");
+    mode = env ? atoi(env) : 0;
+  }
+  q.serp = (tma_fed && (mode >= 2 || (mode == 1 && wide))) ? (mode == 3 ? 2 : 1) : 0;
+}
+
 // L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: off (default) |
 // keep | keepfirst).  A raster band is group_m row-blocks x all column blocks,
 // visited row-block-fastest.  When a band holds more tiles than the 74
@@ -1162,6 +1180,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   // the wide (long-K, TMA-fed) kernels only: gating the gather kernels' ring
   // starves their cp.async warps (C1 layer 1: 5.6 -> 6.7 ms under ncu)
   set_lockstep(q, clusters, WIDE && !has_gather(AM, BMODE));
+  set_serp(q, !has_gather(AM, BMODE), WIDE);
   q.tile_ctr = tile_counter(st, q.sync_chunk > 0);
   if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
   q.prog = q.tile_ctr + 1;

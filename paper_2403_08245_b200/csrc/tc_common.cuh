@@ -61,6 +61,10 @@ struct Params {
   int sync_chunk;   // k-blocks per chunk
   int sync_slack;   // chunks
   int nclusters;
+  // Serpentine K order (tc2, SMOE_TC_SERP): tiles of odd waves (tile index
+  // within its expert / 74) stream their k-blocks last-to-first, so a wave
+  // starts on the K range the previous wave read last.  0 = off.
+  int serp;
   // Head-layout output (staged epilogue, grouped-M, hd_dh > 0): out is the
   // attention core's [batch][h * hd_k][hd_seq][hd_dh] tensor and output row i
   // (slot s = order[i]: token s / hd_k, choice s % hd_k) is scattered into
@@ -346,7 +350,11 @@ struct Tile {
   int64_t k0;     // grouped-K: first bin row
   int64_t k_len;  // reduction length
   int nkb;        // number of BK blocks
+  bool rev;       // k-blocks streamed last-to-first (Params::serp)
 };
+
+// Position (k-block index) of the tile's kb-th streamed k-block.
+__device__ __forceinline__ int kpos(const Tile &tl, int kb) { return tl.rev ? tl.nkb - 1 - kb : kb; }
 
 // Tile t -> (expert, m-block, n-block) with band rasterisation: group_m m-blocks
 // share each B panel while it is hot in L2.  s_start[e] = first tile of expert e.
@@ -388,6 +396,11 @@ __device__ __forceinline__ Tile decode_tile(int64_t t, const Params &p, const in
     tl.k_len = s_off[e + 1] - s_off[e];
   }
   tl.nkb = (int)((tl.k_len + 63) / 64);
+  // waves of 74 tiles (one per CTA pair) counted from the expert's first tile:
+  // a function of the tile's place in its expert only, so the expert-parallel
+  // kernels (a rank's experts, renumbered) reverse exactly the same tiles
+  // (serp 2, A/B: by global tile id / grid pairs instead)
+  tl.rev = p.serp == 1 ? ((local / 74) & 1) : p.serp == 2 ? ((t / p.nclusters) & 1) : false;
   return tl;
 }
 

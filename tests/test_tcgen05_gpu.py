@@ -90,7 +90,7 @@ torch.save((y.cpu(), dw.cpu()), sys.argv[1])
     outs = []
     for ctas in ("2", "1"):
         path = f"/tmp/smoe_tc_{ctas}.pt"
-        env = dict(os.environ, SMOE_TC_CTAS=ctas)
+        env = dict(os.environ, SMOE_TC_CTAS=ctas, SMOE_TC_SERP="0")   # same K order in both engines
         subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300)
         outs.append(torch.load(path))
     (y2, dw2), (y1, dw1) = outs
@@ -180,8 +180,48 @@ torch.save([x.cpu() for x in outs], sys.argv[1])
                          # the wave-lockstep gate only reorders issue in time
                          ("lockstep", {"SMOE_TC_WIDE": "1", "SMOE_TC_SYNC": "2", "SMOE_TC_SYNC_SLACK": "1"})):
         path = str(tmp_path / f"wide_{tag}.pt")
-        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, **env_add), timeout=300)
+        # serpentine K order off: it reverses tiles by their index, which the tile shape changes
+        subprocess.run([sys.executable, "-c", code, path], check=True,
+                       env=dict(os.environ, SMOE_TC_SERP="0", **env_add), timeout=300)
         runs[tag] = torch.load(path)
     for tag in ("wide4", "wide1", "lockstep"):
         for i, (u, v) in enumerate(zip(runs["off"], runs[tag])):
             assert torch.equal(u, v), (tag, i)
+
+
+def test_serpentine_k_order(tmp_path):
+    """SMOE_TC_SERP: tiles of odd 74-tile waves (counted within their expert)
+    stream K last-to-first.  Only the fp32 accumulation order changes: the
+    results match the forward order to rounding, differ somewhere (the reversal
+    ran), and are deterministic run to run."""
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2403_08245_b200 as sm
+torch.manual_seed(4)
+t, k, e, d, de = 8192, 2, 2, 328, 4872       # ~8192 rows per expert: > 74 tiles per expert
+ids = torch.stack([torch.randperm(e)[:k] for _ in range(t)]).cuda()
+r = sm.RoutingResult(ids, torch.rand(t, k, device='cuda'), torch.zeros(t, e, device='cuda'), renormalized=False, validate=False)
+o = sm.compute_grouped_order(r)
+n = t * k
+xg = (torch.rand(n, d, device='cuda') * 2 - 1).bfloat16()
+w = ((torch.rand(e, d, de, device='cuda') * 2 - 1) / 16).bfloat16()
+h = torch.empty(n, de, device='cuda', dtype=torch.bfloat16)
+a = torch.empty_like(h)
+sm.scatter2scatter(xg, w, o, 1, sm.GROUPED_TO_GROUPED, out=h, activation='gelu', act_out=a, engine='tcgen05')
+outs = [h, a, sm.scatter2scatter(h, w, o, 1, sm.GROUPED_TO_SCATTERED, transpose_w=True, engine='tcgen05'),
+        sm.group_xty(xg, h, o, engine='tcgen05'), sm.group_xty(h, xg, o, engine='tcgen05')]
+torch.save([x.cpu() for x in outs], sys.argv[1])
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for tag, serp in (("fwd", "0"), ("serp", "2"), ("serp_again", "2")):
+        path = str(tmp_path / f"serp_{tag}.pt")
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=dict(os.environ, SMOE_TC_SERP=serp),
+                       timeout=300)
+        runs[tag] = torch.load(path)
+    differs = False
+    for i, (u, v, w_) in enumerate(zip(runs["fwd"], runs["serp"], runs["serp_again"])):
+        assert torch.equal(v, w_), i
+        assert _rel(v, u) < 2e-3, (i, _rel(v, u))
+        differs = differs or not torch.equal(u, v)
+    assert differs
