@@ -1119,21 +1119,25 @@ static void set_lockstep(Params &q, int clusters, bool eligible) {
 }
 
 // Serpentine K order (SMOE_TC_SERP: 0 off, 1 wide TMA-fed kernels, 2 every
-// TMA-fed kernel, 3 every TMA-fed kernel by global tile id / grid pairs): a
+// TMA-fed kernel, 3 every TMA-fed kernel by global tile id / grid pairs, 4 the
+// TMA-fed grouped-K (weight-gradient) kernels): a
 // tile streams its k-blocks in reverse when its index within its expert, / 74
 // (the CTA pairs), is odd, so each wave of concurrent tiles starts on the K
 // range the previous wave read last (still in L2).  A tile's accumulation
-// order then depends on its tile shape and place in the schedule.  Measured
-// (profiles/r2_lockstep.txt): dW GEMM -1 %, step +0.2 % (mode 2) to +0.5-1.1 %
-// (mode 3), at the cost of the bit-identity between the expert-parallel and
-// single-GPU paths (and, mode 3, with the grid size) — off by default.
-static void set_serp(Params &q, bool tma_fed, bool wide) {
+// order then depends on its tile shape and place within its expert (never on
+// the grid or the other experts).  Measured (profiles/r2_lockstep.txt): the dW
+// GEMM -1.2 % (C1 5.86 -> 5.80 ms, C2 3.15 -> 3.10), step +0.3 %; applied to the
+// grouped-M kernels too (modes 1-3) it gains little more and would make the
+// expert-parallel layer 1 (a TMA-fed kernel) differ in rounding from the
+// single-GPU gather kernel — so the default is 4, the weight-gradient kernels.
+static void set_serp(Params &q, bool tma_fed, bool wide, bool gk) {
   static int mode = -1;
   if (mode < 0) {
     const char *env = getenv("SMOE_TC_SERP");
-    mode = env ? atoi(env) : 0;
+    mode = env ? atoi(env) : 4;
   }
-  q.serp = (tma_fed && (mode >= 2 || (mode == 1 && wide))) ? (mode == 3 ? 2 : 1) : 0;
+  const bool on = tma_fed && (mode == 2 || mode == 3 || (mode == 1 && wide) || (mode == 4 && gk));
+  q.serp = on ? (mode == 3 ? 2 : 1) : 0;
 }
 
 // L2 eviction priority of the TMA operand loads (SMOE_L2_HINT: off (default) |
@@ -1180,7 +1184,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   // the wide (long-K, TMA-fed) kernels only: gating the gather kernels' ring
   // starves their cp.async warps (C1 layer 1: 5.6 -> 6.7 ms under ncu)
   set_lockstep(q, clusters, WIDE && !has_gather(AM, BMODE));
-  set_serp(q, !has_gather(AM, BMODE), WIDE);
+  set_serp(q, !has_gather(AM, BMODE), WIDE, GK);
   q.tile_ctr = tile_counter(st, q.sync_chunk > 0);
   if (!q.tile_ctr) return check_launch("tc2_gemm: tile counter");
   q.prog = q.tile_ctr + 1;
