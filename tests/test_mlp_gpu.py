@@ -426,3 +426,68 @@ def test_scaled_mlp_random_shapes_vs_oracle(seed):
     absdot = (np.abs(dy).astype(np.float64)[:, None, :] * np.abs(st["y_hat"]).reshape(tokens, k, d)).sum(-1)
     err = np.abs(np_of(gr.dp).astype(np.float64) - want[3])
     assert np.all(err <= 2e-2 * absdot + 1e-6), (float((err / np.maximum(absdot, 1e-30)).max()), case)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_size_token_permutation_equivariance(cfg):
+    """A size-independent property at the full BASELINE shapes: permuting the
+    tokens (and their routing) permutes Y, dX and dp BIT-EXACTLY — each output
+    row is computed from its own slot rows in a fixed K order whatever its place
+    in the expert bins — while dW1 / dW2 (sums over the bins, whose row order
+    changes) agree to fp32 summation-order rounding."""
+    tokens, d, de, e, k = (32768, 4096, 14336, 8, 2) if cfg == "C1" else (32768, 4096, 1792, 64, 8)
+    g = torch.Generator(device="cuda").manual_seed(17)
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / np.sqrt(d)).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / np.sqrt(de)).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    routing = sm.topk_select(torch.softmax(torch.randn(tokens, e, device="cuda", generator=g), 1), k)
+    perm = torch.randperm(tokens, generator=g, device="cuda")
+
+    def run(xx, dyy, ids, p):
+        rt = sm.RoutingResult(ids, p, torch.zeros((tokens, e), device="cuda"), renormalized=True, validate=False)
+        order = sm.compute_grouped_order(rt)
+        y, ctx = sm.smoe_mlp_forward(xx, w1, w2, rt, order)
+        return y, sm.smoe_mlp_backward(ctx, dyy)
+
+    y0, g0 = run(x, dy, routing.expert_idx, routing.p)
+    y1, g1 = run(x[perm].contiguous(), dy[perm].contiguous(), routing.expert_idx[perm].contiguous(),
+                 routing.p[perm].contiguous())
+    assert torch.equal(y1, y0[perm])
+    assert torch.equal(g1.dx, g0.dx[perm])
+    assert torch.equal(g1.dp, g0.dp[perm])
+    assert rel_err(g1.dw1, np_of(g0.dw1)) <= 2e-3
+    assert rel_err(g1.dw2, np_of(g0.dw2)) <= 2e-3
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_full_size_expert_relabel_invariance(cfg):
+    """Relabelling the experts (ids through a permutation sigma, weight stacks
+    permuted to match) moves each expert's bin to another place in the grouped
+    order but keeps its rows and their order: Y, dX, dp and every expert's
+    dW1 / dW2 are bit-identical at the full BASELINE shapes (bin offsets,
+    tile-to-expert mapping and per-expert schedules exercised at size)."""
+    tokens, d, de, e, k = (32768, 4096, 14336, 8, 2) if cfg == "C1" else (32768, 4096, 1792, 64, 8)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    x = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w1 = ((torch.rand((e, d, de), generator=g, device="cuda") * 2 - 1) / np.sqrt(d)).to(torch.bfloat16)
+    w2 = ((torch.rand((e, de, d), generator=g, device="cuda") * 2 - 1) / np.sqrt(de)).to(torch.bfloat16)
+    dy = (torch.rand((tokens, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    logits = torch.randn(tokens, e, device="cuda", generator=g)
+    logits[:, 0] += 1.0                                   # uneven bins
+    routing = sm.topk_select(torch.softmax(logits, 1), k)
+    sigma = torch.randperm(e, generator=g, device="cuda")  # old id -> new id
+    inv = torch.argsort(sigma)
+
+    def run(ids, ww1, ww2):
+        rt = sm.RoutingResult(ids, routing.p, torch.zeros((tokens, e), device="cuda"), renormalized=True,
+                              validate=False)
+        order = sm.compute_grouped_order(rt)
+        y, ctx = sm.smoe_mlp_forward(x, ww1, ww2, rt, order)
+        return y, sm.smoe_mlp_backward(ctx, dy)
+
+    y0, g0 = run(routing.expert_idx, w1, w2)
+    y1, g1 = run(sigma[routing.expert_idx].contiguous(), w1[inv].contiguous(), w2[inv].contiguous())
+    assert torch.equal(y1, y0)
+    assert torch.equal(g1.dx, g0.dx) and torch.equal(g1.dp, g0.dp)
+    assert torch.equal(g1.dw1, g0.dw1[inv]) and torch.equal(g1.dw2, g0.dw2[inv])
